@@ -1,0 +1,232 @@
+// pec_host.cpp — host side of the PEC C ABI: CRC-32C for the persist tier.
+//
+// Replaces the reference's pure-Python, byte-at-a-time table CRC
+// (pkg/src/mocsim/store.py:49-70, ~4.4 MB/s) with the x86 SSE4.2 `crc32`
+// instruction run as three interleaved streams (the instruction has a
+// 3-cycle latency and single-cycle throughput), joined with GF(2) shift
+// operators, and spread over host threads for multi-GB snapshot entries.
+// Semantics are identical to store.crc32c(data, crc): reflected Castagnoli
+// polynomial 0x82F63B78, pre- and post-inversion, chainable.
+
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <thread>
+#include <vector>
+
+#if defined(__x86_64__) || defined(_M_X64)
+#include <nmmintrin.h>
+#define PEC_HAVE_X86 1
+#endif
+
+#include "pec.h"
+
+namespace {
+
+constexpr uint32_t kPoly = 0x82F63B78u;  // reflected Castagnoli
+
+// ---- GF(2) arithmetic modulo the CRC polynomial (reflected bit order) ----
+// Bit 31 holds x^0.  mul(a, b) = a*b mod P.
+uint32_t gf2_mul(uint32_t a, uint32_t b) {
+  uint32_t prod = 0;
+  for (uint32_t bit = 1u << 31; bit != 0; bit >>= 1) {
+    if (a & bit) prod ^= b;
+    b = (b & 1u) ? (b >> 1) ^ kPoly : b >> 1;
+  }
+  return prod;
+}
+
+struct Tables {
+  uint32_t byte_table[8][256];  // slicing-by-8 software tables
+  uint32_t x2k[64];             // x^(2^k) mod P
+  uint32_t shift_block[4][256]; // "append kBlock zero bytes" operator
+  Tables();
+  // x^(8 * nbytes) mod P
+  uint32_t xpow_bytes(uint64_t nbytes) const {
+    uint32_t acc = 1u << 31;  // 1
+    unsigned k = 3;           // 8 bits per byte = 2^3
+    while (nbytes) {
+      if (nbytes & 1u) acc = gf2_mul(x2k[k & 63], acc);
+      nbytes >>= 1;
+      ++k;
+    }
+    return acc;
+  }
+};
+
+constexpr size_t kBlock = 8192;  // per-stream block of the 3-way interleave
+
+Tables::Tables() {
+  for (uint32_t i = 0; i < 256; ++i) {
+    uint32_t c = i;
+    for (int b = 0; b < 8; ++b) c = (c & 1u) ? (c >> 1) ^ kPoly : c >> 1;
+    byte_table[0][i] = c;
+  }
+  for (uint32_t i = 0; i < 256; ++i)
+    for (int s = 1; s < 8; ++s)
+      byte_table[s][i] = (byte_table[s - 1][i] >> 8) ^ byte_table[0][byte_table[s - 1][i] & 0xFFu];
+  uint32_t p = 1u << 30;  // x^1
+  for (int k = 0; k < 64; ++k) {
+    x2k[k] = p;
+    p = gf2_mul(p, p);
+  }
+  const uint32_t op = xpow_bytes(kBlock);
+  for (int j = 0; j < 4; ++j)
+    for (uint32_t b = 0; b < 256; ++b) shift_block[j][b] = gf2_mul(op, b << (8 * j));
+}
+
+const Tables& tables() {
+  static const Tables t;
+  return t;
+}
+
+inline uint32_t shift_by_block(const Tables& t, uint32_t reg) {
+  return t.shift_block[0][reg & 0xFFu] ^ t.shift_block[1][(reg >> 8) & 0xFFu] ^
+         t.shift_block[2][(reg >> 16) & 0xFFu] ^ t.shift_block[3][reg >> 24];
+}
+
+// Register update (no inversion) over [p, p+n), software slicing-by-8.
+uint32_t reg_update_sw(const Tables& t, uint32_t reg, const uint8_t* p, size_t n) {
+  while (n && (reinterpret_cast<uintptr_t>(p) & 7u)) {
+    reg = (reg >> 8) ^ t.byte_table[0][(reg ^ *p++) & 0xFFu];
+    --n;
+  }
+  while (n >= 8) {
+    uint64_t w;
+    memcpy(&w, p, 8);
+    w ^= reg;
+    reg = t.byte_table[7][w & 0xFF] ^ t.byte_table[6][(w >> 8) & 0xFF] ^
+          t.byte_table[5][(w >> 16) & 0xFF] ^ t.byte_table[4][(w >> 24) & 0xFF] ^
+          t.byte_table[3][(w >> 32) & 0xFF] ^ t.byte_table[2][(w >> 40) & 0xFF] ^
+          t.byte_table[1][(w >> 48) & 0xFF] ^ t.byte_table[0][w >> 56];
+    p += 8;
+    n -= 8;
+  }
+  while (n--) reg = (reg >> 8) ^ t.byte_table[0][(reg ^ *p++) & 0xFFu];
+  return reg;
+}
+
+#ifdef PEC_HAVE_X86
+__attribute__((target("sse4.2")))
+uint32_t reg_update_hw(const Tables& t, uint32_t reg, const uint8_t* p, size_t n) {
+  uint64_t r0 = reg;
+  while (n && (reinterpret_cast<uintptr_t>(p) & 7u)) {
+    r0 = _mm_crc32_u8((uint32_t)r0, *p++);
+    --n;
+  }
+  // three independent streams over consecutive kBlock blocks, then
+  // r = shift(shift(r0) ^ r1) ^ r2
+  while (n >= 3 * kBlock) {
+    uint64_t r1 = 0, r2 = 0;
+    const uint8_t* a = p;
+    const uint8_t* b = p + kBlock;
+    const uint8_t* c = p + 2 * kBlock;
+    for (size_t i = 0; i < kBlock; i += 8) {
+      uint64_t wa, wb, wc;
+      memcpy(&wa, a + i, 8);
+      memcpy(&wb, b + i, 8);
+      memcpy(&wc, c + i, 8);
+      r0 = _mm_crc32_u64(r0, wa);
+      r1 = _mm_crc32_u64(r1, wb);
+      r2 = _mm_crc32_u64(r2, wc);
+    }
+    r0 = shift_by_block(t, (uint32_t)r0) ^ (uint32_t)r1;
+    r0 = shift_by_block(t, (uint32_t)r0) ^ (uint32_t)r2;
+    p += 3 * kBlock;
+    n -= 3 * kBlock;
+  }
+  while (n >= 8) {
+    uint64_t w;
+    memcpy(&w, p, 8);
+    r0 = _mm_crc32_u64(r0, w);
+    p += 8;
+    n -= 8;
+  }
+  while (n--) r0 = _mm_crc32_u8((uint32_t)r0, *p++);
+  return (uint32_t)r0;
+}
+
+bool have_sse42() {
+  static const bool ok = __builtin_cpu_supports("sse4.2");
+  return ok;
+}
+#endif
+
+uint32_t crc_impl(const void* data, size_t n, uint32_t crc) {
+  const Tables& t = tables();
+  const uint8_t* p = static_cast<const uint8_t*>(data);
+  uint32_t reg = ~crc;
+#ifdef PEC_HAVE_X86
+  if (have_sse42()) return ~reg_update_hw(t, reg, p, n);
+#endif
+  return ~reg_update_sw(t, reg, p, n);
+}
+
+uint32_t combine_impl(uint32_t crc_a, uint32_t crc_b, uint64_t len_b) {
+  if (len_b == 0) return crc_a;
+  const Tables& t = tables();
+  return gf2_mul(t.xpow_bytes(len_b), crc_a) ^ crc_b;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t pec_crc32c(const void* data, size_t n, uint32_t crc) {
+  if (n == 0) return crc;
+  if (data == nullptr) return crc;
+  return crc_impl(data, n, crc);
+}
+
+uint32_t pec_crc32c_combine(uint32_t crc_a, uint32_t crc_b, uint64_t len_b) {
+  return combine_impl(crc_a, crc_b, len_b);
+}
+
+int pec_crc32c_many(const void* base, const uint64_t* offs, const uint64_t* lens, int n,
+                    uint32_t* out, int threads) {
+  if (n < 0 || (n > 0 && (base == nullptr || offs == nullptr || lens == nullptr || out == nullptr)))
+    return PEC_E_INVAL;
+  if (n == 0) return PEC_OK;
+  if (threads < 1) threads = 1;
+  const uint8_t* b = static_cast<const uint8_t*>(base);
+
+  // Cut every region into pieces of <= kPiece bytes; threads take pieces
+  // round-robin by index; each region's CRC is the ordered combine of its
+  // pieces' CRCs.
+  constexpr uint64_t kPiece = 64ull << 20;
+  struct Piece { int region; uint64_t off, len; uint32_t crc; };
+  std::vector<Piece> pieces;
+  std::vector<size_t> first(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    first[i] = pieces.size();
+    uint64_t o = 0;
+    do {
+      const uint64_t l = std::min<uint64_t>(kPiece, lens[i] - o);
+      pieces.push_back(Piece{i, offs[i] + o, l, 0});
+      o += l;
+    } while (o < lens[i]);
+  }
+  first[n] = pieces.size();
+  const int nt = (int)std::min<size_t>((size_t)threads, pieces.size());
+  auto work = [&](int tid) {
+    for (size_t k = (size_t)tid; k < pieces.size(); k += (size_t)nt)
+      pieces[k].crc = pieces[k].len ? crc_impl(b + pieces[k].off, pieces[k].len, 0) : 0u;
+  };
+  if (nt <= 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    pool.reserve(nt);
+    for (int t = 0; t < nt; ++t) pool.emplace_back(work, t);
+    for (auto& th : pool) th.join();
+  }
+  for (int i = 0; i < n; ++i) {
+    uint32_t c = 0;
+    for (size_t k = first[i]; k < first[i + 1]; ++k) c = combine_impl(c, pieces[k].crc, pieces[k].len);
+    out[i] = c;
+  }
+  return PEC_OK;
+}
+
+}  // extern "C"

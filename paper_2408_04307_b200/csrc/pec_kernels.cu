@@ -1,0 +1,587 @@
+// pec_kernels.cu — sm_100a kernels of the PEC snapshot path + their C ABI.
+//
+// Kernels (see DESIGN.md for the roofline of each):
+//   token_hist_kernel        per-expert token histogram of one iteration's
+//                            router ids, capacity clamp, int64 accumulation
+//                            (reference: simulator.py:88-95, :560-567)
+//   select_sequential_kernel window selection (selector.py:21-32)
+//   select_load_aware_kernel top-K by (-unsaved, id) + mark_saved
+//                            (selector.py:86-100, simulator.py:339-354)
+//   copy_vec_kernel          gather/scatter engine, LDG/STG.128
+//   copy_bulk_kernel         gather/scatter engine, TMA bulk (cp.async.bulk)
+//                            global->smem->global ring
+// pack and unpack are the same engines over a table whose src/dst roles are
+// swapped (pack: state -> staging, unpack: staging -> state).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pec.h"
+
+namespace {
+
+constexpr int kMaxExperts = 4096;
+
+// ------------------------------------------------------------------------
+// device attribute cache (not state: a pure function of the device id)
+// ------------------------------------------------------------------------
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (cached[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cached[dev] = n;
+  }
+  return cached[dev];
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PEC_OK : PEC_E_CUDA;
+}
+
+// ------------------------------------------------------------------------
+// (a) token histogram
+// ------------------------------------------------------------------------
+// grid = (blocks_per_layer, L).  Each CTA histograms a contiguous slice of
+// one layer's ids into shared memory using warp aggregation (__match_any_sync
+// groups the lanes holding the same id; the group leader adds the popcount),
+// then folds its histogram into scratch with global atomics.  The last CTA
+// to finish (ticket in scratch[L*E]) applies the per-iteration capacity
+// clamp, accumulates into the int64 counters and re-zeroes scratch — one
+// launch per iteration, no host round trip.
+constexpr int kHistThreads = 256;
+constexpr int kHistUnroll = 8;
+
+__global__ void __launch_bounds__(kHistThreads)
+token_hist_kernel(const int32_t* __restrict__ idx, int L, int64_t n, int E,
+                  const int64_t* __restrict__ cap, int64_t* __restrict__ counters,
+                  int tiers, int64_t* __restrict__ delivered,
+                  uint32_t* __restrict__ scratch) {
+  extern __shared__ uint32_t hist[];  // E + 1 (slot E collects ignored ids)
+  const int layer = blockIdx.y;
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * per;
+  const int64_t hi = lo + per < n ? lo + per : n;
+  const int32_t* row = idx + (int64_t)layer * n;
+  const unsigned lane = threadIdx.x & 31u;
+
+  // The trip count depends only on (lo, hi), uniform across the CTA, so the
+  // full-mask __match_any_sync below always sees converged warps.
+  for (int64_t base = lo; base < hi; base += (int64_t)kHistThreads * kHistUnroll) {
+    int v[kHistUnroll];
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t i = base + (int64_t)u * kHistThreads + threadIdx.x;
+      v[u] = i < hi ? __ldg(row + i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int key = (unsigned)v[u] < (unsigned)E ? v[u] : E;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      if (lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[key], (uint32_t)__popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const uint32_t c = hist[e];
+    if (c) atomicAdd(&scratch[(int64_t)layer * E + e], c);
+  }
+
+  // last-CTA-done: fence our atomics, take a ticket
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t total = gridDim.x * gridDim.y;
+    const uint32_t t = atomicAdd(&scratch[(int64_t)L * E], 1u);
+    is_last = (t == total - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const int64_t le = (int64_t)L * E;
+  for (int64_t j = threadIdx.x; j < le; j += blockDim.x) {
+    const int64_t c = (int64_t)atomicExch(&scratch[j], 0u);  // read via L2 and clear
+    const int64_t cl = cap ? (c < cap[j / E] ? c : cap[j / E]) : c;
+    if (cl) {
+      for (int t = 0; t < tiers; ++t) counters[(int64_t)t * le + j] += cl;
+      if (delivered) delivered[j] += cl;
+    }
+  }
+  if (threadIdx.x == 0) atomicExch(&scratch[le], 0u);
+}
+
+// ------------------------------------------------------------------------
+// (b) selection
+// ------------------------------------------------------------------------
+__global__ void select_sequential_kernel(int64_t c, int L, int E, int width, int stride,
+                                         int32_t* __restrict__ out) {
+  const int W = width < E ? width : E;
+  const int64_t total = (int64_t)L * W;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(t / W);
+    const int j = (int)(t % W);
+    int v;
+    if (width >= E) {
+      v = j;
+    } else {
+      // window {(m + c*stride + k) mod E : k < W}, emitted sorted ascending:
+      // the wrapped part [0, s+W-E) first, then [s, min(E, s+W)).
+      const int64_t s64 = ((int64_t)m + (c % E) * (int64_t)(stride % E)) % E;
+      const int s = (int)((s64 + E) % E);
+      const int wrap = s + W - E > 0 ? s + W - E : 0;
+      v = j < wrap ? j : s + (j - wrap);
+    }
+    out[t] = v;
+  }
+}
+
+// One warp per layer.  Candidate e is selected iff fewer than K candidates
+// beat it under (count desc, id asc).  A per-warp shared bitmap over expert
+// ids turns the selection into an ascending compaction (ballot + popc).
+constexpr int kSelWarps = 4;
+
+__global__ void __launch_bounds__(32 * kSelWarps)
+select_load_aware_kernel(int64_t* __restrict__ counters, int L, int E, int K,
+                         const int32_t* __restrict__ pool, int P,
+                         int32_t* __restrict__ out, int zero_selected) {
+  extern __shared__ uint8_t sel_bits[];  // kSelWarps * E
+  const int warp_in_block = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int layer = blockIdx.x * kSelWarps + warp_in_block;
+  if (layer >= L) return;  // warp-uniform
+  uint8_t* bits = sel_bits + (int64_t)warp_in_block * E;
+  int64_t* cnt = counters + (int64_t)layer * E;
+  const int32_t* pl = pool ? pool + (int64_t)layer * P : nullptr;
+  const int ncand = pool ? P : E;
+
+  for (int e = lane; e < E; e += 32) bits[e] = 0;
+  __syncwarp();
+
+  int nvalid = 0;  // valid candidates in the pool (all lanes agree)
+  for (int i = 0; i < ncand; ++i) {
+    const int e = pl ? pl[i] : i;
+    nvalid += (e >= 0 && e < E);
+  }
+  const int kk = K < nvalid ? K : nvalid;
+
+  for (int i0 = 0; i0 < ncand; i0 += 32) {
+    const int i = i0 + lane;
+    int e = -1;
+    if (i < ncand) e = pl ? pl[i] : i;
+    if (e >= 0 && e < E) {
+      const int64_t ce = cnt[e];
+      int rank = 0;
+      for (int j = 0; j < ncand && rank < kk; ++j) {
+        const int ej = pl ? pl[j] : j;
+        if (ej < 0 || ej >= E) continue;
+        const int64_t cj = cnt[ej];
+        rank += (cj > ce) || (cj == ce && ej < e);
+      }
+      if (rank < kk) bits[e] = 1;
+    }
+  }
+  __syncwarp();
+
+  int32_t* o = out + (int64_t)layer * K;
+  int written = 0;
+  for (int e0 = 0; e0 < E; e0 += 32) {
+    const int e = e0 + lane;
+    const bool s = e < E && bits[e];
+    const unsigned m = __ballot_sync(0xffffffffu, s);
+    if (s) {
+      const int pos = written + __popc(m & ((1u << lane) - 1u));
+      o[pos] = e;
+      if (zero_selected) cnt[e] = 0;
+    }
+    written += __popc(m);
+  }
+  for (int j = written + lane; j < K; j += 32) o[j] = -1;
+}
+
+// ------------------------------------------------------------------------
+// (c)/(d) gather/scatter engines
+// ------------------------------------------------------------------------
+__device__ __forceinline__ int find_desc(const pec_copy_desc* __restrict__ d, int n, uint64_t ch) {
+  // largest i with first_chunk[i] <= ch (empty descriptors share the next
+  // one's first_chunk and are skipped by taking the largest such i)
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&d[mid].first_chunk) <= ch) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
+  asm volatile("st.global.cs.v4.s32 [%0], {%1, %2, %3, %4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// Byte-exact copy of [s, s+len) -> [t, t+len) by one CTA.  Fast path when
+// s == t (mod 16): <16 head bytes, a 16-byte-vector body with UNROLL loads in
+// flight per thread, <16 tail bytes.  Otherwise a word or byte loop.
+template <int THREADS, int UNROLL>
+__device__ __forceinline__ void cta_copy(const uint8_t* __restrict__ s, uint8_t* __restrict__ t,
+                                         uint64_t len) {
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(s);
+  const uintptr_t ta = reinterpret_cast<uintptr_t>(t);
+  if (((sa ^ ta) & 15u) == 0) {
+    uint64_t head = (16u - (sa & 15u)) & 15u;
+    if (head > len) head = len;
+    if (threadIdx.x < head) t[threadIdx.x] = s[threadIdx.x];
+    const int4* vs = reinterpret_cast<const int4*>(s + head);
+    int4* vt = reinterpret_cast<int4*>(t + head);
+    const uint64_t nv = (len - head) >> 4;
+    for (uint64_t v = threadIdx.x; v < nv; v += (uint64_t)THREADS * UNROLL) {
+      int4 r[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint64_t k = v + (uint64_t)u * THREADS;
+        if (k < nv) r[u] = ld_stream(vs + k);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint64_t k = v + (uint64_t)u * THREADS;
+        if (k < nv) st_stream(vt + k, r[u]);
+      }
+    }
+    const uint64_t ts = head + (nv << 4);
+    const uint64_t tail = len - ts;
+    if (threadIdx.x < tail) t[ts + threadIdx.x] = s[ts + threadIdx.x];
+  } else if (((sa ^ ta) & 3u) == 0) {
+    uint64_t head = (4u - (sa & 3u)) & 3u;
+    if (head > len) head = len;
+    if (threadIdx.x < head) t[threadIdx.x] = s[threadIdx.x];
+    const uint32_t* ws = reinterpret_cast<const uint32_t*>(s + head);
+    uint32_t* wt = reinterpret_cast<uint32_t*>(t + head);
+    const uint64_t nw = (len - head) >> 2;
+    for (uint64_t w = threadIdx.x; w < nw; w += THREADS) wt[w] = __ldg(ws + w);
+    const uint64_t ts = head + (nw << 2);
+    if (threadIdx.x < len - ts) t[ts + threadIdx.x] = s[ts + threadIdx.x];
+  } else {
+    for (uint64_t b = threadIdx.x; b < len; b += THREADS) t[b] = s[b];
+  }
+}
+
+constexpr int kVecThreads = 256;
+constexpr int kVecUnroll = 8;
+
+__global__ void __launch_bounds__(kVecThreads)
+copy_vec_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total, int lg) {
+  for (uint64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
+    const int i = find_desc(d, n, ch);
+    const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << lg;
+    const uint64_t nb = __ldg(&d[i].nbytes);
+    const uint64_t span = 1ull << lg;
+    const uint64_t len = nb - off < span ? nb - off : span;
+    const uint8_t* s = reinterpret_cast<const uint8_t*>(__ldg(&d[i].src) + off);
+    uint8_t* t = reinterpret_cast<uint8_t*>(__ldg(&d[i].dst) + off);
+    cta_copy<kVecThreads, kVecUnroll>(s, t, len);
+  }
+}
+
+// ---- TMA bulk engine -----------------------------------------------------
+// One elected thread per CTA streams the CTA's chunks through a ring of
+// kStages shared-memory stages: cp.async.bulk global->smem completes on the
+// stage's mbarrier, then cp.async.bulk smem->global (bulk_group) drains it.
+// A stage is refilled only after `cp.async.bulk.wait_group.read` confirms
+// the store that last read it has consumed the shared memory.  The 16-byte
+// aligned body of each chunk goes through TMA; its (<16 B) unaligned head and
+// tail, and any chunk whose src/dst are not congruent mod 16, are copied by
+// the other warps with plain loads/stores in parallel.
+constexpr int kBulkThreads = 128;
+constexpr int kBulkStages = 6;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}"
+      :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      :: "r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(gmem), "r"(smem_u32(smem)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct ChunkView {
+  const uint8_t* s;
+  uint8_t* t;
+  uint64_t len;
+  uint64_t head;   // bytes before the 16-byte aligned body
+  uint64_t body;   // multiple of 16, 0 when not congruent
+};
+
+__device__ __forceinline__ ChunkView chunk_view(const pec_copy_desc* __restrict__ d, int n,
+                                                uint64_t ch, int lg) {
+  ChunkView v;
+  const int i = find_desc(d, n, ch);
+  const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << lg;
+  const uint64_t nb = __ldg(&d[i].nbytes);
+  const uint64_t span = 1ull << lg;
+  v.len = nb - off < span ? nb - off : span;
+  v.s = reinterpret_cast<const uint8_t*>(__ldg(&d[i].src) + off);
+  v.t = reinterpret_cast<uint8_t*>(__ldg(&d[i].dst) + off);
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(v.s);
+  const uintptr_t ta = reinterpret_cast<uintptr_t>(v.t);
+  if (((sa ^ ta) & 15u) == 0) {
+    uint64_t head = (16u - (sa & 15u)) & 15u;
+    if (head > v.len) head = v.len;
+    v.head = head;
+    v.body = (v.len - head) & ~uint64_t(15);
+  } else {
+    v.head = 0;
+    v.body = 0;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(kBulkThreads, 1)
+copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total, int lg) {
+  extern __shared__ __align__(128) uint8_t ring[];  // kBulkStages << lg
+  __shared__ __align__(8) uint64_t bars[kBulkStages];
+  const uint32_t stage_bytes = 1u << lg;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (threadIdx.x == 0) {
+    // ---- single-thread TMA driver -------------------------------------
+    // j-th chunk of this CTA = blockIdx.x + j * gridDim.x
+    const uint64_t mine = blockIdx.x < total ? (total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    uint64_t body_of[kBulkStages];
+    uint8_t* dst_of[kBulkStages];
+    // prologue: fill the ring
+    const uint64_t pre = mine < (uint64_t)kBulkStages ? mine : (uint64_t)kBulkStages;
+    for (uint64_t j = 0; j < pre; ++j) {
+      const ChunkView v = chunk_view(d, n, blockIdx.x + j * gridDim.x, lg);
+      const int s = (int)j;
+      body_of[s] = v.body;
+      dst_of[s] = v.t + v.head;
+      if (v.body) {
+        mbar_expect_tx(&bars[s], (uint32_t)v.body);
+        bulk_g2s(ring + (uint64_t)s * stage_bytes, v.s + v.head, (uint32_t)v.body, &bars[s]);
+      } else {
+        mbar_arrive(&bars[s]);  // keep the stage's phase sequence in step
+      }
+    }
+    for (uint64_t j = 0; j < mine; ++j) {
+      const int s = (int)(j % kBulkStages);
+      const uint32_t parity = (uint32_t)((j / kBulkStages) & 1u);
+      mbar_wait(&bars[s], parity);
+      if (body_of[s]) {
+        bulk_s2g(dst_of[s], ring + (uint64_t)s * stage_bytes, (uint32_t)body_of[s]);
+      }
+      bulk_commit();  // one group per chunk (possibly empty) keeps counts exact
+      // refill the stage consumed one step earlier with chunk j-1+kStages
+      if (j >= 1) {
+        const uint64_t jn = j - 1 + kBulkStages;
+        if (jn < mine) {
+          bulk_wait_read<1>();  // the store of chunk j-1 has read its stage
+          const int sp = (int)((j - 1) % kBulkStages);
+          const ChunkView v = chunk_view(d, n, blockIdx.x + jn * gridDim.x, lg);
+          body_of[sp] = v.body;
+          dst_of[sp] = v.t + v.head;
+          if (v.body) {
+            mbar_expect_tx(&bars[sp], (uint32_t)v.body);
+            bulk_g2s(ring + (uint64_t)sp * stage_bytes, v.s + v.head, (uint32_t)v.body, &bars[sp]);
+          } else {
+            mbar_arrive(&bars[sp]);
+          }
+        }
+      }
+    }
+    bulk_wait_all();
+  } else {
+    // ---- edge workers: unaligned heads/tails and incongruent chunks -----
+    const int wid = threadIdx.x - 32;  // warps 1..3 (96 threads)
+    if (wid >= 0) {
+      for (uint64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
+        const ChunkView v = chunk_view(d, n, ch, lg);
+        if (v.body == 0 && v.len > 0) {
+          // incongruent or tiny chunk: plain copy by the 96 edge threads
+          const uintptr_t sa = reinterpret_cast<uintptr_t>(v.s);
+          const uintptr_t ta = reinterpret_cast<uintptr_t>(v.t);
+          if (((sa ^ ta) & 3u) == 0 && v.len >= 8) {
+            const uint64_t head = (4u - (sa & 3u)) & 3u;
+            if ((uint64_t)wid < head) v.t[wid] = v.s[wid];
+            const uint32_t* ws = reinterpret_cast<const uint32_t*>(v.s + head);
+            uint32_t* wt = reinterpret_cast<uint32_t*>(v.t + head);
+            const uint64_t nw = (v.len - head) >> 2;
+            for (uint64_t w = wid; w < nw; w += kBulkThreads - 32) wt[w] = __ldg(ws + w);
+            const uint64_t ts = head + (nw << 2);
+            if ((uint64_t)wid < v.len - ts) v.t[ts + wid] = v.s[ts + wid];
+          } else {
+            for (uint64_t b = wid; b < v.len; b += kBulkThreads - 32) v.t[b] = v.s[b];
+          }
+        } else {
+          if ((uint64_t)wid < v.head) v.t[wid] = v.s[wid];
+          const uint64_t ts = v.head + v.body;
+          if ((uint64_t)wid < v.len - ts) v.t[ts + wid] = v.s[ts + wid];
+        }
+      }
+    }
+  }
+}
+
+int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, int lg, int mode, void* stream) {
+  if (n < 0 || lg < 12 || lg > 24) return PEC_E_INVAL;
+  if (total == 0 || n == 0) return PEC_OK;
+  if (descs == nullptr) return PEC_E_INVAL;
+  if (mode < 0 || mode > 2) return PEC_E_INVAL;
+  const int sms = sm_count();
+  cudaStream_t st = as_stream(stream);
+  if (mode == 2) {
+    const int smem = kBulkStages << lg;
+    if (smem > 227 * 1024) return PEC_E_RANGE;
+    if (cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return PEC_E_CUDA;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_bulk_kernel, kBulkThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)sms * per_sm;
+    if (grid > total) grid = total;
+    copy_bulk_kernel<<<(unsigned)grid, kBulkThreads, smem, st>>>(descs, n, total, lg);
+    return launch_status();
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_vec_kernel, kVecThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = (uint64_t)sms * per_sm;
+  if (grid > total) grid = total;
+  copy_vec_kernel<<<(unsigned)grid, kVecThreads, 0, st>>>(descs, n, total, lg);
+  return launch_status();
+}
+
+}  // namespace
+
+// ========================================================================
+// C ABI
+// ========================================================================
+extern "C" {
+
+int pec_abi_version(void) { return PEC_ABI_VERSION; }
+
+const char* pec_strerror(int code) {
+  switch (code) {
+    case PEC_OK: return "ok";
+    case PEC_E_INVAL: return "invalid argument";
+    case PEC_E_CUDA: return "CUDA launch/runtime error";
+    case PEC_E_RANGE: return "size exceeds a kernel limit";
+    default: return "unknown error";
+  }
+}
+
+int pec_token_hist(const int32_t* idx, int L, int64_t n_per_layer, int E,
+                   const int64_t* cap, int64_t* counters, int tiers,
+                   int64_t* delivered, uint32_t* scratch, void* stream) {
+  if (L < 1 || L > 65535 || E < 1 || n_per_layer < 0 || tiers < 0) return PEC_E_INVAL;
+  if (E > kMaxExperts) return PEC_E_RANGE;
+  if (scratch == nullptr || (n_per_layer > 0 && idx == nullptr)) return PEC_E_INVAL;
+  if (tiers > 0 && counters == nullptr) return PEC_E_INVAL;
+  const int sms = sm_count();
+  // enough CTAs to fill the GPU, each with >= one full unrolled sweep of ids
+  int64_t per_layer = (int64_t)sms * 4 / L;
+  const int64_t sweep = (int64_t)kHistThreads * kHistUnroll;
+  const int64_t need = (n_per_layer + sweep - 1) / sweep;
+  if (per_layer > need) per_layer = need;
+  if (per_layer < 1) per_layer = 1;
+  dim3 grid((unsigned)per_layer, (unsigned)L);
+  const size_t smem = (size_t)(E + 1) * sizeof(uint32_t);
+  token_hist_kernel<<<grid, kHistThreads, smem, as_stream(stream)>>>(
+      idx, L, n_per_layer, E, cap, counters, tiers, delivered, scratch);
+  return launch_status();
+}
+
+int pec_select_sequential(int64_t c, int L, int E, int width, int stride,
+                          int32_t* out, void* stream) {
+  if (L < 1 || E < 1 || width < 1 || stride < 0 || c < 0 || out == nullptr) return PEC_E_INVAL;
+  const int W = width < E ? width : E;
+  const int64_t total = (int64_t)L * W;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 1024) blocks = 1024;
+  select_sequential_kernel<<<blocks, 256, 0, as_stream(stream)>>>(c, L, E, width, stride, out);
+  return launch_status();
+}
+
+int pec_select_load_aware(int64_t* counters, int L, int E, int K,
+                          const int32_t* pool, int P, int32_t* out,
+                          int zero_selected, void* stream) {
+  if (L < 1 || E < 1 || K < 1 || counters == nullptr || out == nullptr) return PEC_E_INVAL;
+  if (pool != nullptr && P < 0) return PEC_E_INVAL;
+  if (E > kMaxExperts) return PEC_E_RANGE;
+  const int blocks = (L + kSelWarps - 1) / kSelWarps;
+  const size_t smem = (size_t)kSelWarps * E;
+  select_load_aware_kernel<<<blocks, 32 * kSelWarps, smem, as_stream(stream)>>>(
+      counters, L, E, K, pool, pool ? P : 0, out, zero_selected);
+  return launch_status();
+}
+
+int pec_pack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
+             int chunk_log2, int mode, void* stream) {
+  return launch_copy(descs, n, total_chunks, chunk_log2, mode == 0 ? 1 : mode, stream);
+}
+
+int pec_unpack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
+               int chunk_log2, int mode, void* stream) {
+  return launch_copy(descs, n, total_chunks, chunk_log2, mode == 0 ? 1 : mode, stream);
+}
+
+int64_t pec_plan_chunks(pec_copy_desc* host_descs, int n, int chunk_log2) {
+  if (n < 0 || chunk_log2 < 12 || chunk_log2 > 24) return PEC_E_INVAL;
+  if (n > 0 && host_descs == nullptr) return PEC_E_INVAL;
+  uint64_t acc = 0;
+  const uint64_t span = 1ull << chunk_log2;
+  for (int i = 0; i < n; ++i) {
+    host_descs[i].first_chunk = acc;
+    acc += (host_descs[i].nbytes + span - 1) / span;
+  }
+  return (int64_t)acc;
+}
+
+}  // extern "C"

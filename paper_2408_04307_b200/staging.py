@@ -1,0 +1,108 @@
+"""Staging layout: where each planned byte range lands in the snapshot buffer.
+
+A rank's snapshot is its ordered `RangeAssignment` list for the phase
+(reference `planner.py:263-295`).  The pack kernel gathers those ranges, in
+that order, into one contiguous device staging buffer, which the copy engine
+then drains into a pinned host buffer with the *same* layout; the persist
+thread writes each entry file straight out of the host buffer.
+
+Entry i starts at the first offset >= the end of entry i-1 that is congruent
+to its source address modulo 256 (``STAGE_ALIGN``).  Unit images are
+256-byte aligned in the arena (`arena.py`), so source and destination of
+every copy share their alignment: the kernel streams aligned 16-byte vectors
+(or TMA bulk copies) from the first full granule to the last, with only
+sub-16-byte heads/tails at byte-granular range boundaries (the floor-split
+expert weight parts, planner.py:188-195).  Padding is at most 255 B per
+entry; entry files carry exact bytes.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .device import DEFAULT_CHUNK_LOG2, DESC_DTYPE, plan_chunks
+from .planner import RangeAssignment
+
+STAGE_ALIGN = 256
+
+
+@dataclass(frozen=True)
+class StagedEntry:
+    store_key: str
+    unit_key: str
+    start: int          # byte range [start, stop) of the unit image
+    stop: int
+    part: Optional[int]
+    rank: int
+    src_offset: int     # arena offset of byte `start`
+    stage_offset: int   # staging offset of byte `start`
+
+    @property
+    def nbytes(self) -> int:
+        return self.stop - self.start
+
+
+class StagingLayout:
+    """Placement of one rank's ranges in the staging / host snapshot buffer."""
+
+    def __init__(self, entries: Sequence[StagedEntry], nbytes: int):
+        self.entries: Tuple[StagedEntry, ...] = tuple(entries)
+        self.nbytes = nbytes
+        self.payload_bytes = sum(e.nbytes for e in self.entries)
+        self._by_store_key = {e.store_key: e for e in self.entries}
+
+    @classmethod
+    def build(cls, ranges: Iterable[RangeAssignment], arena, rank: int = 0,
+              align: int = STAGE_ALIGN) -> "StagingLayout":
+        out: List[StagedEntry] = []
+        pos = 0
+        for a in ranges:
+            if a.stop <= a.start:
+                continue
+            src = arena.slot(a.key).offset + a.start
+            off = pos + ((src - pos) % align)
+            out.append(StagedEntry(a.store_key, a.key, a.start, a.stop, a.part, rank, src, off))
+            pos = off + (a.stop - a.start)
+        return cls(out, pos)
+
+    def entry(self, store_key: str) -> StagedEntry:
+        return self._by_store_key[store_key]
+
+    def __len__(self) -> int:
+        return len(self.entries)
+
+    # -- descriptor tables ------------------------------------------------------
+    def descriptors(self, state_base: int, stage_base: int, reverse: bool = False,
+                    chunk_log2: int = DEFAULT_CHUNK_LOG2,
+                    select: Optional[Iterable[str]] = None) -> Tuple[np.ndarray, int]:
+        """Host `pec_copy_desc` table (pack: state -> stage; reverse:
+        stage -> state) and its total chunk count.  ``select`` limits the
+        table to the given store keys (partial restores)."""
+        keys = None if select is None else set(select)
+        ents = [e for e in self.entries if keys is None or e.store_key in keys]
+        table = np.zeros(len(ents), dtype=DESC_DTYPE)
+        for i, e in enumerate(ents):
+            s = state_base + e.src_offset
+            t = stage_base + e.stage_offset
+            table[i]["src"], table[i]["dst"] = (t, s) if reverse else (s, t)
+            table[i]["nbytes"] = e.nbytes
+        total = plan_chunks(table, chunk_log2)
+        return table, total
+
+
+class DeviceTable:
+    """A descriptor table resident in device memory, ready for pec_pack."""
+
+    def __init__(self, table: np.ndarray, total_chunks: int, device,
+                 chunk_log2: int = DEFAULT_CHUNK_LOG2):
+        import torch
+        self.n = len(table)
+        self.total_chunks = total_chunks
+        self.chunk_log2 = chunk_log2
+        raw = torch.from_numpy(table.view(np.uint8).copy()) if self.n else \
+            torch.zeros(DESC_DTYPE.itemsize, dtype=torch.uint8)
+        self.tensor = raw.view(torch.int64).to(device)
+        self.nbytes_moved = int(table["nbytes"].sum()) if self.n else 0

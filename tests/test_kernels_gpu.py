@@ -1,0 +1,206 @@
+"""Parity of the sm_100a kernels (through the C ABI) against the CPU oracle."""
+
+import numpy as np
+import pytest
+
+from conftest import make_layout
+from oracle import pec_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+# ---------------------------------------------------------------------------
+# (a) token histogram
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("L,n,E", [(1, 1, 1), (4, 4096 * 2, 8), (6, 16384 * 2, 8),
+                                   (12, 3000, 16), (32, 32768, 8), (3, 100003, 64),
+                                   (2, 77, 4096)])
+def test_token_hist_matches_bincount_with_cap(dev, L, n, E):
+    import torch
+    from paper_2408_04307_b200 import device as D
+    rng = np.random.default_rng(L * 1000 + E)
+    counters = torch.zeros((2, L, E), dtype=torch.int64, device=dev)
+    delivered = torch.zeros((L, E), dtype=torch.int64, device=dev)
+    scratch = torch.zeros(L * E + 1, dtype=torch.int32, device=dev)
+    want = np.zeros((L, E), dtype=np.int64)
+    for it in range(3):
+        # skewed ids with some out-of-range (dropped) entries
+        ids = np.minimum(rng.zipf(1.3, size=(L, n)) - 1, E + 2).astype(np.int32)
+        ids[rng.random((L, n)) < 0.01] = -1
+        cap = np.array([O.capacity(1.25, n, E) for _ in range(L)], dtype=np.int64)
+        cap[0] = max(1, cap[0] // 3)
+        D.token_hist(torch.from_numpy(ids).to(dev), counters, scratch,
+                     cap=torch.from_numpy(cap).to(dev), delivered=delivered)
+        want += O.route_counts(ids, E, cap)
+    torch.cuda.synchronize()
+    assert np.array_equal(counters[0].cpu().numpy(), want)
+    assert np.array_equal(counters[1].cpu().numpy(), want)
+    assert np.array_equal(delivered.cpu().numpy(), want)
+    assert int(scratch.abs().sum()) == 0  # left zeroed for the next call
+
+
+def test_token_hist_reproduces_reference_zipf_routing(dev):
+    """Explicit ids drawn from the reference's PCG64 Zipf stream, counted on
+    device, equal the reference route_tokens counts (golden)."""
+    import json
+    import torch
+    from conftest import GOLDEN
+    from paper_2408_04307_b200 import device as D
+    g = json.loads((GOLDEN / "routing.json").read_text())
+    for case in g["zipf"]:
+        L, E, total = case["layers"], case["experts"], case["total"]
+        ids = np.stack([O.zipf_router_ids(case["seed"], case["iteration"], m, E, total,
+                                          case["s"]) for m in range(L)])
+        cap = O.capacity(case["capacity_factor"], total, E)
+        counters = torch.zeros((1, L, E), dtype=torch.int64, device=dev)
+        scratch = torch.zeros(L * E + 1, dtype=torch.int32, device=dev)
+        capt = None if cap is None else torch.full((L,), cap, dtype=torch.int64, device=dev)
+        D.token_hist(torch.from_numpy(ids).to(dev), counters, scratch, cap=capt)
+        assert counters[0].cpu().tolist() == case["counts"], case
+
+
+# ---------------------------------------------------------------------------
+# (b) selection
+# ---------------------------------------------------------------------------
+
+def test_select_sequential_matches_window(dev):
+    import torch
+    from paper_2408_04307_b200 import device as D
+    for E in (1, 3, 4, 8, 16, 64):
+        for width in sorted({1, 2, 3, E // 2 or 1, E, E + 1}):
+            for stride in sorted({0, 1, 2, 3, E}):
+                for c in (0, 1, 5, 17, 1000003):
+                    L = 7
+                    w = min(width, E)
+                    out = torch.full((L, w), -7, dtype=torch.int32, device=dev)
+                    D.select_sequential(c, L, E, width, stride, out)
+                    got = out.cpu().tolist()
+                    want = [O.select_window(c, m, E, width, stride) for m in range(L)]
+                    assert got == want, (E, width, stride, c)
+
+
+@pytest.mark.parametrize("E", [1, 4, 8, 16, 33, 256])
+def test_select_load_aware_ties_pools_and_reset(dev, E):
+    import torch
+    from paper_2408_04307_b200 import device as D
+    rng = np.random.default_rng(E)
+    L = 9
+    for trial in range(20):
+        hi = 3 if trial % 2 else 10**12  # many ties vs. wide range
+        snap = rng.integers(0, hi, size=(L, E)).astype(np.int64)
+        pers = rng.integers(0, hi, size=(L, E)).astype(np.int64)
+        k_s = int(rng.integers(1, E + 1))
+        k_p = int(rng.integers(1, k_s + 1))
+        ss, ps, snap_after, pers_after = O.two_tier_load_aware(snap, pers, k_s, k_p)
+        ds, dp = torch.from_numpy(snap).to(dev), torch.from_numpy(pers).to(dev)
+        out_s = torch.empty((L, k_s), dtype=torch.int32, device=dev)
+        out_p = torch.empty((L, k_p), dtype=torch.int32, device=dev)
+        D.select_load_aware(ds, k_s, out_s, zero_selected=True)
+        D.select_load_aware(dp, k_p, out_p, pool=out_s, zero_selected=True)
+        assert out_s.cpu().tolist() == ss
+        assert out_p.cpu().tolist() == ps
+        assert np.array_equal(ds.cpu().numpy(), snap_after)
+        assert np.array_equal(dp.cpu().numpy(), pers_after)
+
+
+def test_select_load_aware_golden(dev):
+    import json
+    import torch
+    from conftest import GOLDEN
+    from paper_2408_04307_b200 import device as D
+    g = json.loads((GOLDEN / "selection.json").read_text())
+    for case in g["load_aware"]:
+        counts = torch.tensor([case["counts"]], dtype=torch.int64, device=dev)
+        k = case["k"]
+        out = torch.empty((1, k), dtype=torch.int32, device=dev)
+        pool = None
+        if case["pool"] is not None:
+            pool = torch.tensor([case["pool"]], dtype=torch.int32, device=dev)
+        D.select_load_aware(counts, k, out, pool=pool)
+        got = [e for e in out.cpu().tolist()[0] if e >= 0]
+        assert got == case["selected"], case
+
+
+# ---------------------------------------------------------------------------
+# (c)/(d) pack and unpack
+# ---------------------------------------------------------------------------
+
+def _random_copies(rng, state_size, n, max_len, congruent):
+    copies, pos = [], 0
+    for _ in range(n):
+        ln = int(rng.integers(0, max_len))
+        src = int(rng.integers(0, state_size - ln))
+        if congruent:
+            dst = pos + ((src - pos) % 256)
+        else:
+            dst = pos + int(rng.integers(0, 64))
+        copies.append((src, dst, ln))
+        pos = dst + ln
+    return copies, pos
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("chunk_log2", [12, 15, 18])
+@pytest.mark.parametrize("congruent", [True, False])
+def test_pack_unpack_random_ranges(dev, mode, chunk_log2, congruent):
+    import torch
+    from paper_2408_04307_b200 import device as D
+    rng = np.random.default_rng(chunk_log2 * 10 + mode + (100 if congruent else 0))
+    size = 8 << 20
+    state = torch.randint(0, 256, (size,), dtype=torch.uint8, device=dev)
+    copies, stage_size = _random_copies(rng, size, 300, 200_000, congruent)
+    copies += [(5, stage_size + 3, 0), (size - 17, stage_size + 7, 17)]
+    stage_size += 7 + 17
+    staging = torch.zeros(stage_size + 64, dtype=torch.uint8, device=dev)
+    table = np.zeros(len(copies), dtype=D.DESC_DTYPE)
+    for i, (s, t, n) in enumerate(copies):
+        table[i] = (state.data_ptr() + s, staging.data_ptr() + t, n, 0)
+    total = D.plan_chunks(table, chunk_log2)
+    dt = torch.from_numpy(table.view(np.uint8).copy()).view(torch.int64).to(dev)
+    D.pack(dt, len(table), total, chunk_log2, mode)
+    torch.cuda.synchronize()
+    host_state = state.cpu().numpy()
+    want = O.pack(host_state, copies, stage_size + 64)
+    assert np.array_equal(staging.cpu().numpy(), want)
+
+    # unpack into a zeroed state image: exactly the copied ranges come back
+    back = torch.zeros_like(state)
+    rtable = table.copy()
+    for i, (s, t, n) in enumerate(copies):
+        rtable[i]["src"], rtable[i]["dst"] = staging.data_ptr() + t, back.data_ptr() + s
+    total = D.plan_chunks(rtable, chunk_log2)
+    rt = torch.from_numpy(rtable.view(np.uint8).copy()).view(torch.int64).to(dev)
+    D.unpack(rt, len(rtable), total, chunk_log2, mode)
+    torch.cuda.synchronize()
+    want_back = O.unpack(want, copies, np.zeros(size, dtype=np.uint8))
+    assert np.array_equal(back.cpu().numpy(), want_back)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_pack_plan_phases_bit_exact(dev, mode):
+    """Every phase of an adaptive K=1 plan on a 2-EP-group layout with an odd
+    expert size (byte-granular weight parts) packs bit-exactly."""
+    import torch
+    from paper_2408_04307_b200 import PecConfig, plan_adaptive, plan_equal
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.staging import DeviceTable, StagingLayout
+    from paper_2408_04307_b200 import device as D
+    layout = make_layout(n_experts=4, dp=4, ep=2, epp=100_001, p_ne=30_001, other=37,
+                         modules=(("a", 10_000), ("b", 10_001), ("c", 10_000)))
+    arena = StateArena(layout, ranks=range(4), device=dev)
+    host_state = arena.buffer.cpu().numpy()
+    for plan in (plan_adaptive(layout, PecConfig(k_pec=1)),
+                 plan_equal(layout, PecConfig(k_pec=2, k_snapshot=2, k_persist=1))):
+        for phase in plan.assignments:
+            for rank, ranges in phase.items():
+                st = StagingLayout.build(ranges, arena, rank)
+                staging = torch.zeros(st.nbytes + 1, dtype=torch.uint8, device=dev)
+                table, total = st.descriptors(arena.base_address, staging.data_ptr())
+                dtab = DeviceTable(table, total, dev)
+                D.pack(dtab.tensor, dtab.n, dtab.total_chunks, mode=mode)
+                torch.cuda.synchronize()
+                got = staging.cpu().numpy()
+                copies = [(e.src_offset, e.stage_offset, e.nbytes) for e in st.entries]
+                assert np.array_equal(got, O.pack(host_state, copies, st.nbytes + 1))
+                assert st.payload_bytes == plan.workload_bytes[plan.assignments.index(phase)][rank]
