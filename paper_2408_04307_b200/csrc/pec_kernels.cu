@@ -378,11 +378,39 @@ __device__ __forceinline__ ChunkView chunk_view(const pec_copy_desc* __restrict_
   return v;
 }
 
+// Pipeline items are pieces of <= kStageBytes of a chunk's aligned body:
+// item j of this CTA is piece (j % P) of its (j / P)-th chunk, P = pieces per
+// chunk, so chunk sizes above one stage simply yield more items.
+constexpr int kStageLog2 = 15;
+
+struct Piece {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint32_t bytes;  // 0 => nothing to move (phase still advanced)
+};
+
+__device__ __forceinline__ Piece piece_of(const pec_copy_desc* __restrict__ d, int n, int lg,
+                                          uint64_t j, uint32_t per_chunk, int piece_log2) {
+  const uint64_t jc = j / per_chunk;
+  const uint32_t jp = (uint32_t)(j % per_chunk);
+  const ChunkView v = chunk_view(d, n, blockIdx.x + jc * gridDim.x, lg);
+  Piece p;
+  const uint64_t lo = (uint64_t)jp << piece_log2;
+  const uint64_t hi = lo + (1ull << piece_log2);
+  const uint64_t end = hi < v.body ? hi : v.body;
+  p.bytes = end > lo ? (uint32_t)(end - lo) : 0u;
+  p.src = v.s + v.head + lo;
+  p.dst = v.t + v.head + lo;
+  return p;
+}
+
 __global__ void __launch_bounds__(kBulkThreads, 1)
 copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total, int lg) {
-  extern __shared__ __align__(128) uint8_t ring[];  // kBulkStages << lg
+  extern __shared__ __align__(128) uint8_t ring[];  // kBulkStages * stage
   __shared__ __align__(8) uint64_t bars[kBulkStages];
-  const uint32_t stage_bytes = 1u << lg;
+  const int piece_log2 = lg < kStageLog2 ? lg : kStageLog2;
+  const uint32_t stage_bytes = 1u << piece_log2;
+  const uint32_t per_chunk = 1u << (lg - piece_log2);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[s], 1);
@@ -392,48 +420,32 @@ copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total, int
 
   if (threadIdx.x == 0) {
     // ---- single-thread TMA driver -------------------------------------
-    // j-th chunk of this CTA = blockIdx.x + j * gridDim.x
-    const uint64_t mine = blockIdx.x < total ? (total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    uint64_t body_of[kBulkStages];
+    const uint64_t chunks = blockIdx.x < total ? (total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint64_t items = chunks * per_chunk;
+    uint32_t bytes_of[kBulkStages];
     uint8_t* dst_of[kBulkStages];
-    // prologue: fill the ring
-    const uint64_t pre = mine < (uint64_t)kBulkStages ? mine : (uint64_t)kBulkStages;
-    for (uint64_t j = 0; j < pre; ++j) {
-      const ChunkView v = chunk_view(d, n, blockIdx.x + j * gridDim.x, lg);
-      const int s = (int)j;
-      body_of[s] = v.body;
-      dst_of[s] = v.t + v.head;
-      if (v.body) {
-        mbar_expect_tx(&bars[s], (uint32_t)v.body);
-        bulk_g2s(ring + (uint64_t)s * stage_bytes, v.s + v.head, (uint32_t)v.body, &bars[s]);
+    auto issue = [&](uint64_t j, int s) {
+      const Piece p = piece_of(d, n, lg, j, per_chunk, piece_log2);
+      bytes_of[s] = p.bytes;
+      dst_of[s] = p.dst;
+      if (p.bytes) {
+        mbar_expect_tx(&bars[s], p.bytes);
+        bulk_g2s(ring + (uint64_t)s * stage_bytes, p.src, p.bytes, &bars[s]);
       } else {
         mbar_arrive(&bars[s]);  // keep the stage's phase sequence in step
       }
-    }
-    for (uint64_t j = 0; j < mine; ++j) {
+    };
+    const uint64_t pre = items < (uint64_t)kBulkStages ? items : (uint64_t)kBulkStages;
+    for (uint64_t j = 0; j < pre; ++j) issue(j, (int)j);
+    for (uint64_t j = 0; j < items; ++j) {
       const int s = (int)(j % kBulkStages);
-      const uint32_t parity = (uint32_t)((j / kBulkStages) & 1u);
-      mbar_wait(&bars[s], parity);
-      if (body_of[s]) {
-        bulk_s2g(dst_of[s], ring + (uint64_t)s * stage_bytes, (uint32_t)body_of[s]);
-      }
-      bulk_commit();  // one group per chunk (possibly empty) keeps counts exact
-      // refill the stage consumed one step earlier with chunk j-1+kStages
-      if (j >= 1) {
-        const uint64_t jn = j - 1 + kBulkStages;
-        if (jn < mine) {
-          bulk_wait_read<1>();  // the store of chunk j-1 has read its stage
-          const int sp = (int)((j - 1) % kBulkStages);
-          const ChunkView v = chunk_view(d, n, blockIdx.x + jn * gridDim.x, lg);
-          body_of[sp] = v.body;
-          dst_of[sp] = v.t + v.head;
-          if (v.body) {
-            mbar_expect_tx(&bars[sp], (uint32_t)v.body);
-            bulk_g2s(ring + (uint64_t)sp * stage_bytes, v.s + v.head, (uint32_t)v.body, &bars[sp]);
-          } else {
-            mbar_arrive(&bars[sp]);
-          }
-        }
+      mbar_wait(&bars[s], (uint32_t)((j / kBulkStages) & 1u));
+      if (bytes_of[s]) bulk_s2g(dst_of[s], ring + (uint64_t)s * stage_bytes, bytes_of[s]);
+      bulk_commit();  // one group per item (possibly empty) keeps counts exact
+      // refill the stage consumed one step earlier with item j-1+kStages
+      if (j >= 1 && j - 1 + kBulkStages < items) {
+        bulk_wait_read<1>();  // the store of item j-1 has read its stage
+        issue(j - 1 + kBulkStages, (int)((j - 1) % kBulkStages));
       }
     }
     bulk_wait_all();
@@ -477,8 +489,7 @@ int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, int lg, int m
   const int sms = sm_count();
   cudaStream_t st = as_stream(stream);
   if (mode == 2) {
-    const int smem = kBulkStages << lg;
-    if (smem > 227 * 1024) return PEC_E_RANGE;
+    const int smem = kBulkStages << (lg < kStageLog2 ? lg : kStageLog2);
     if (cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return PEC_E_CUDA;
     int per_sm = 1;

@@ -1,0 +1,441 @@
+"""The B200 two-level snapshot path: pack -> HBM staging -> D2H -> pinned
+host buffer -> persist thread, driven by the reference's buffer state machine.
+
+`DeviceCheckpointEngine` is the reference `CheckpointEngine` (engine.py)
+with the byte movement the reference only models
+(`transfer_us(snap_bytes, snapshot_bandwidth)`, simulator.py:57-61, 434-438)
+made real:
+
+  begin_snapshot   pack stream waits for the compute stream (the state is
+                   consistent there), one `pec_pack` launch gathers every
+                   local rank's planned ranges into the HBM staging buffer,
+                   then the copy stream drains staging into the pinned host
+                   buffer whose id the state machine handed out.
+  wait_pack        the compute stream waits for the pack before the next
+                   optimizer step may modify the state (the only
+                   consistency-critical part; the drain overlaps training).
+  complete_snapshot  after the drain's event: SNAPSHOTTED = bytes in host RAM.
+  start_persist    a background thread writes the persisted subset straight
+                   out of the host buffer (CRC-32C via libpec), multi-rank
+                   commits through a gloo group (rank files, then rank 0
+                   publishes meta/manifest/COMPLETE).
+  complete_persist publishes and rotates the buffer roles.
+
+`PecCheckpointer` is the training-loop driver, the counterpart of
+`Simulation._trigger_checkpoint` / `step` (simulator.py:396-457, 546-576):
+token counting every iteration, selection + plan + snapshot every
+``i_ckpt`` iterations, asynchronous completion via `poll`.
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from concurrent.futures import Future, ThreadPoolExecutor
+from dataclasses import dataclass, field
+from typing import Dict, Iterable, List, Mapping, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import device as D
+from .arena import StateArena
+from .engine import Buffer, CheckpointEngine, NoFreeBufferError
+from .planner import (
+    ADAPTIVE_PEC,
+    BASELINE,
+    EQUAL_FULL,
+    EQUAL_PEC,
+    LOAD_AWARE,
+    PecConfig,
+    PhaseAssignment,
+    ShardPlan,
+    build_phase_assignment,
+    plan_adaptive,
+    plan_baseline,
+    plan_equal,
+)
+from .selector import select_window
+from .staging import DeviceTable, StagingLayout
+from .store import StoreEntry
+from .topology import RankLayout
+
+
+@dataclass
+class _Inflight:
+    """Device-side record of one buffer's snapshot."""
+    layouts: Dict[int, StagingLayout]     # local rank -> layout (offsets within its region)
+    region: Dict[int, int]                # local rank -> byte offset of its region
+    nbytes: int
+    pack_done: object = None
+    drain_done: object = None
+    t_begin: float = 0.0
+
+
+class DeviceCheckpointEngine(CheckpointEngine):
+    """Reference CheckpointEngine + real snapshot/persist bytes on B200."""
+
+    def __init__(self, layout: RankLayout, store, arena: StateArena,
+                 ranks: Optional[Sequence[int]] = None, n_buffers: int = 3,
+                 pack_mode: int = D.MODE_AUTO, chunk_log2: int = D.DEFAULT_CHUNK_LOG2,
+                 control_group=None, persist_threads: int = 1):
+        import torch
+        super().__init__(layout, store, n_buffers)
+        self.arena = arena
+        self.device = arena.device
+        self.ranks = tuple(ranks) if ranks is not None else arena.ranks
+        self.pack_mode = pack_mode
+        self.chunk_log2 = chunk_log2
+        self.group = control_group
+        self.pack_stream = torch.cuda.Stream(device=self.device)
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.staging = None
+        self.host: List[Optional[object]] = [None] * n_buffers
+        self._inflight: Dict[int, _Inflight] = {}       # buffer_id -> record
+        self._tables: Dict[Tuple, Tuple[DeviceTable, Dict[int, StagingLayout], Dict[int, int], int]] = {}
+        self._staging_free = None
+        self._persist_pool = ThreadPoolExecutor(max_workers=persist_threads,
+                                                thread_name_prefix="pec-persist")
+        self._persist: Dict[int, Tuple[Future, List[StoreEntry]]] = {}
+        self.stats = {"pack_ms": [], "drain_ms": [], "persist_s": [], "snap_bytes": []}
+
+    # -- buffers -----------------------------------------------------------------
+    def _ensure_staging(self, nbytes: int):
+        import torch
+        if self.staging is None or self.staging.numel() < nbytes:
+            if self.staging is not None:
+                torch.cuda.current_stream(self.device).synchronize()
+                self.pack_stream.synchronize()
+                self.copy_stream.synchronize()
+            self.staging = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._tables.clear()  # addresses changed
+
+    def _ensure_host(self, buffer_id: int, nbytes: int):
+        import torch
+        h = self.host[buffer_id]
+        if h is None or h.numel() < nbytes:
+            self.host[buffer_id] = torch.empty(max(nbytes, 256), dtype=torch.uint8, pin_memory=True)
+        return self.host[buffer_id]
+
+    def reserve(self, nbytes: int) -> None:
+        """Pre-allocate staging and all host buffers (pinning is slow: do it
+        once, before training)."""
+        self._ensure_staging(nbytes)
+        for i in range(len(self.host)):
+            self._ensure_host(i, nbytes)
+
+    # -- plan -> device table ------------------------------------------------------
+    def _table_for(self, assignment: PhaseAssignment, key=None):
+        if key is not None and key in self._tables:
+            return self._tables[key]
+        layouts, region, pos = {}, {}, 0
+        for r in self.ranks:
+            st = StagingLayout.build(assignment.get(r, ()), self.arena, r)
+            layouts[r], region[r] = st, pos
+            pos += (st.nbytes + 255) // 256 * 256
+        self._ensure_staging(pos)
+        tables = [layouts[r].descriptors(self.arena.base_address,
+                                         self.staging.data_ptr() + region[r],
+                                         chunk_log2=self.chunk_log2)[0] for r in self.ranks]
+        table = np.concatenate(tables) if tables else np.zeros(0, dtype=D.DESC_DTYPE)
+        total = D.plan_chunks(table, self.chunk_log2)
+        entry = (DeviceTable(table, total, self.device, self.chunk_log2), layouts, region, pos)
+        if key is not None:
+            self._tables[key] = entry
+        return entry
+
+    # -- snapshot --------------------------------------------------------------------
+    def begin_snapshot(self, iteration: int, checkpoint_index: int,
+                       assignment: PhaseAssignment, plan_key=None, compute_stream=None) -> Buffer:
+        import torch
+        buf = super().begin_snapshot(iteration, checkpoint_index, assignment)
+        try:
+            table, layouts, region, nbytes = self._table_for(assignment, plan_key)
+            host = self._ensure_host(buf.buffer_id, nbytes)
+        except Exception:
+            buf.clear()
+            self.next_version -= 1
+            raise
+        compute = compute_stream or torch.cuda.current_stream(self.device)
+        rec = _Inflight(layouts, region, nbytes, t_begin=time.perf_counter())
+        ps, cs = self.pack_stream, self.copy_stream
+        ps.wait_stream(compute)                       # state is consistent here
+        if self._staging_free is not None:
+            ps.wait_event(self._staging_free)         # previous drain read staging
+        start = torch.cuda.Event(enable_timing=True)
+        rec.pack_done = torch.cuda.Event(enable_timing=True)
+        start.record(ps)
+        D.pack(table.tensor, table.n, table.total_chunks, table.chunk_log2, self.pack_mode,
+               stream=ps)
+        rec.pack_done.record(ps)
+        rec.pack_start = start
+        cs.wait_event(rec.pack_done)
+        rec.drain_done = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(cs):
+            host[:nbytes].copy_(self.staging[:nbytes], non_blocking=True)
+        rec.drain_done.record(cs)
+        self._staging_free = rec.drain_done
+        self._inflight[buf.buffer_id] = rec
+        self.stats["snap_bytes"].append(sum(l.payload_bytes for l in layouts.values()))
+        return buf
+
+    def wait_pack(self, buf: Optional[Buffer] = None, stream=None) -> None:
+        """Make ``stream`` (default: current) wait for the pack of ``buf`` (or
+        the latest snapshot) before it modifies the state."""
+        import torch
+        rec = self._inflight.get(buf.buffer_id) if buf is not None else \
+            (self._inflight[self.buffers.snapshotting.buffer_id]
+             if self.buffers.snapshotting is not None else None)
+        if rec is not None:
+            (stream or torch.cuda.current_stream(self.device)).wait_event(rec.pack_done)
+
+    def snapshot_ready(self, buf: Buffer) -> bool:
+        rec = self._inflight.get(buf.buffer_id)
+        return rec is None or rec.drain_done.query()
+
+    def complete_snapshot(self, buf: Buffer) -> Optional[Buffer]:
+        rec = self._inflight.get(buf.buffer_id)
+        if rec is not None:
+            rec.drain_done.synchronize()
+            self.stats["pack_ms"].append(rec.pack_start.elapsed_time(rec.pack_done))
+            self.stats["drain_ms"].append(rec.pack_done.elapsed_time(rec.drain_done))
+        return super().complete_snapshot(buf)
+
+    # -- host bytes ---------------------------------------------------------------------
+    def entry_view(self, buf: Buffer, rank: int, store_key: str) -> memoryview:
+        rec = self._inflight[buf.buffer_id]
+        st = rec.layouts[rank]
+        e = st.entry(store_key)
+        off = rec.region[rank] + e.stage_offset
+        host = self.host[buf.buffer_id].numpy()
+        return memoryview(host[off:off + e.nbytes])
+
+    def payloads(self, buf: Buffer, entries: Iterable[StoreEntry]) -> Dict[str, memoryview]:
+        return {e.store_key: self.entry_view(buf, e.rank, e.store_key) for e in entries
+                if e.rank in self.ranks}
+
+    def has_bytes(self, buf: Buffer) -> bool:
+        return buf.buffer_id in self._inflight
+
+    # -- persist --------------------------------------------------------------------------
+    def _write(self, buf: Buffer, entries: List[StoreEntry]) -> float:
+        """Write this process's entry files; multi-process: gather rows, rank
+        0 publishes (single-writer-identical files), everyone syncs."""
+        t0 = time.perf_counter()
+        local = [e for e in entries if e.rank in self.ranks]
+        pay = self.payloads(buf, local)
+        version, it, c = buf.version, buf.iteration, buf.checkpoint_index
+        if self.group is None:
+            self.store.check_version(version)
+            rows = self.store.write_entries(version, it, local, payloads=pay)
+            self.store.publish(version, it, c, entries, rows)
+        else:
+            import torch.distributed as dist
+            rows = self.store.write_entries(version, it, local, payloads=pay)
+            gathered = [None] * dist.get_world_size(self.group)
+            dist.all_gather_object(gathered, rows, group=self.group)
+            if dist.get_rank(self.group) == 0:
+                all_rows = [r for part in gathered for r in part]
+                self.store.publish(version, it, c, entries, all_rows)
+            dist.barrier(group=self.group)
+        return time.perf_counter() - t0
+
+    def start_persist(self, buf: Buffer, entries: List[StoreEntry]) -> Future:
+        fut = self._persist_pool.submit(self._write, buf, list(entries))
+        self._persist[buf.buffer_id] = (fut, list(entries))
+        return fut
+
+    def persist_ready(self, buf: Buffer) -> bool:
+        job = self._persist.get(buf.buffer_id)
+        return job is None or job[0].done()
+
+    def finish_persist(self, buf: Buffer) -> Optional[Buffer]:
+        fut, _ = self._persist.pop(buf.buffer_id)
+        self.stats["persist_s"].append(fut.result())
+        return self.buffers.complete_persist(buf)
+
+    def complete_persist(self, buf: Buffer, entries: List[StoreEntry]) -> Optional[Buffer]:
+        """Synchronous persist (reference signature, engine.py:195-198)."""
+        if buf.buffer_id in self._persist:
+            return self.finish_persist(buf)
+        if not self.has_bytes(buf):
+            return super().complete_persist(buf, entries)  # metadata-only buffer
+        self.stats["persist_s"].append(self._write(buf, entries))
+        return self.buffers.complete_persist(buf)
+
+    def on_fault(self, failed_nodes: Iterable[int]) -> None:
+        for fut, _ in self._persist.values():
+            try:
+                fut.result()
+            except Exception:  # noqa: BLE001 - an interrupted persist leaves no version
+                pass
+        self._persist.clear()
+        super().on_fault(failed_nodes)
+
+    def close(self) -> None:
+        self._persist_pool.shutdown(wait=True)
+
+
+class PecCheckpointer:
+    """Training-loop driver of the PEC snapshot path (one per rank process).
+
+    Mirrors the checkpoint parts of `Simulation` (simulator.py:309-457,
+    546-576) with real bytes: ``step(iteration, router_ids)`` counts tokens and,
+    every ``i_ckpt`` iterations, selects experts (on device), plans, and
+    starts the snapshot; ``poll()`` moves completed drains/persists through
+    the state machine.
+    """
+
+    def __init__(self, layout: RankLayout, arena: StateArena, store, pec: Optional[PecConfig],
+                 strategy: str = EQUAL_PEC, i_ckpt: int = 10, ranks: Optional[Sequence[int]] = None,
+                 counters=None, group=None, control_group=None, n_buffers: int = 3,
+                 pack_mode: int = D.MODE_AUTO, chunk_log2: int = D.DEFAULT_CHUNK_LOG2,
+                 async_persist: bool = True):
+        self.layout = layout
+        self.arena = arena
+        self.pec = pec
+        self.strategy = strategy
+        self.i_ckpt = i_ckpt
+        self.group = group
+        self.engine = DeviceCheckpointEngine(layout, store, arena, ranks, n_buffers, pack_mode,
+                                             chunk_log2, control_group)
+        self.counters = counters
+        self.async_persist = async_persist
+        self.persist_sel: Dict[int, Dict[int, frozenset]] = {}
+        self._plan: Optional[ShardPlan] = None
+        self.stall_s = 0.0
+        if pec is not None and pec.selection == LOAD_AWARE:
+            if strategy == ADAPTIVE_PEC:
+                from .topology import SpecValidationError
+                raise SpecValidationError("adaptive_pec requires sequential selection",
+                                          "load-aware selection is not periodic")
+            if counters is None:
+                raise ValueError("load-aware selection needs DeviceTokenCounters")
+
+    # -- plans --------------------------------------------------------------------
+    def plan(self) -> Optional[ShardPlan]:
+        if self._plan is None and (self.pec is None or self.pec.selection != LOAD_AWARE):
+            if self.pec is None:
+                self._plan = plan_baseline(self.layout) if self.strategy == BASELINE \
+                    else plan_equal(self.layout)
+            else:
+                seq = PecConfig(k_pec=self.pec.k_snapshot, k_snapshot=self.pec.k_snapshot,
+                                k_persist=self.pec.k_persist)
+                self._plan = plan_adaptive(self.layout, seq) if self.strategy == ADAPTIVE_PEC \
+                    else plan_equal(self.layout, seq)
+        return self._plan
+
+    def max_snapshot_bytes(self) -> int:
+        """Upper bound of this process's staging bytes over all phases."""
+        plan = self.plan()
+        ranks = self.engine.ranks
+        if plan is not None:
+            return max(sum((StagingLayout.build(ph.get(r, ()), self.arena, r).nbytes + 255)
+                           // 256 * 256 for r in ranks) for ph in plan.assignments)
+        # load-aware: the heaviest due set is every expert a rank holds
+        full = {m: frozenset(range(self.layout.model.experts_per_layer))
+                for m in range(self.layout.model.num_moe_layers)}
+        ph = build_phase_assignment(self.layout, full, self.strategy)
+        return sum((StagingLayout.build(ph.get(r, ()), self.arena, r).nbytes + 255) // 256 * 256
+                   for r in ranks)
+
+    def selections(self, c: int):
+        """(snapshot sets, persist sets) per layer for checkpoint c
+        (simulator.py:339-354)."""
+        L, n = self.layout.model.num_moe_layers, self.layout.model.experts_per_layer
+        if self.pec is None:
+            full = frozenset(range(n))
+            return {m: full for m in range(L)}, {m: full for m in range(L)}
+        k_s, k_p = self.pec.k_snapshot, self.pec.k_persist
+        if self.pec.selection == LOAD_AWARE:
+            snap_d, pers_d = self.counters.select(k_s, k_p, group=self.group)
+            snap_h, pers_h = snap_d.cpu().tolist(), pers_d.cpu().tolist()
+            return ({m: frozenset(e for e in snap_h[m] if e >= 0) for m in range(L)},
+                    {m: frozenset(e for e in pers_h[m] if e >= 0) for m in range(L)})
+        return ({m: select_window(c, m, n, k_s, k_p) for m in range(L)},
+                {m: select_window(c, m, n, k_p, k_p) for m in range(L)})
+
+    # -- the loop ----------------------------------------------------------------
+    def step(self, iteration: int, router_ids=None) -> Optional[Buffer]:
+        if router_ids is not None and self.counters is not None:
+            self.counters.add_iteration(router_ids)
+        self.poll()
+        if iteration % self.i_ckpt == 0:
+            return self.checkpoint(iteration)
+        return None
+
+    def checkpoint(self, iteration: int) -> Buffer:
+        c = iteration // self.i_ckpt - 1
+        snap_sel, persist_sel = self.selections(c)
+        plan = self.plan()
+        if plan is not None:
+            phase = plan.phase_of(c)
+            assignment, key = plan.assignments[phase], ("phase", phase)
+        else:
+            assignment, key = build_phase_assignment(self.layout, snap_sel, self.strategy), None
+        while True:
+            try:
+                # one snapshot at a time: wait for the previous drain
+                snapping = self.engine.buffers.snapshotting
+                if snapping is not None:
+                    t0 = time.perf_counter()
+                    self._complete(snapping)
+                    self.stall_s += time.perf_counter() - t0
+                buf = self.engine.begin_snapshot(iteration, c, assignment, plan_key=key)
+                break
+            except NoFreeBufferError:
+                t0 = time.perf_counter()
+                if not self._wait_one_persist():
+                    raise
+                self.stall_s += time.perf_counter() - t0
+        self.persist_sel[buf.version] = persist_sel
+        return buf
+
+    def wait_pack(self, stream=None) -> None:
+        self.engine.wait_pack(stream=stream)
+
+    def _complete(self, buf: Buffer) -> None:
+        promoted = self.engine.complete_snapshot(buf)
+        if promoted is not None:
+            self._start_persist(promoted)
+
+    def _start_persist(self, buf: Buffer) -> None:
+        entries = self.engine.persist_entries(buf, self.persist_sel[buf.version])
+        if self.async_persist:
+            self.engine.start_persist(buf, entries)
+        else:
+            nxt = self.engine.complete_persist(buf, entries)
+            if nxt is not None:
+                self._start_persist(nxt)
+
+    def _wait_one_persist(self) -> bool:
+        p = self.engine.buffers.persisting
+        if p is None:
+            return False
+        nxt = self.engine.finish_persist(p)
+        if nxt is not None:
+            self._start_persist(nxt)
+        return True
+
+    def poll(self) -> None:
+        snapping = self.engine.buffers.snapshotting
+        if snapping is not None and self.engine.snapshot_ready(snapping):
+            self._complete(snapping)
+        p = self.engine.buffers.persisting
+        while p is not None and self.engine.persist_ready(p) and p.buffer_id in self.engine._persist:
+            nxt = self.engine.finish_persist(p)
+            if nxt is not None:
+                self._start_persist(nxt)
+            p = self.engine.buffers.persisting
+
+    def finish(self) -> None:
+        """Drain all in-flight snapshot and persist work."""
+        snapping = self.engine.buffers.snapshotting
+        if snapping is not None:
+            self._complete(snapping)
+        while self.engine.buffers.persisting is not None:
+            if not self._wait_one_persist():
+                break
+
+    def close(self) -> None:
+        self.finish()
+        self.engine.close()

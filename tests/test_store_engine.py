@@ -1,0 +1,243 @@
+"""Store format, CRC-32C and recovery decisions vs. the reference (CPU)."""
+
+import hashlib
+import json
+import random
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, make_layout
+from paper_2408_04307_b200 import ClusterSpec, ModelSpec, ParallelSpec, PecConfig, build_layout, plan_equal
+from paper_2408_04307_b200.engine import (
+    FREE,
+    PERSISTING,
+    RECOVERY,
+    SNAPSHOTTED,
+    SNAPSHOTTING,
+    CheckpointEngine,
+    NoFreeBufferError,
+    TripleBufferSet,
+    UnrecoverableStateError,
+)
+from paper_2408_04307_b200.selector import select_window
+from paper_2408_04307_b200.store import (
+    ChecksumMismatchError,
+    CrashPoint,
+    DiskStore,
+    IncompleteVersionError,
+    MemoryStore,
+    StoreEntry,
+    StoreError,
+    TruncatingInjector,
+    crc32c,
+    entry_payload,
+)
+
+STORE = json.loads((GOLDEN / "store.json").read_text())
+RECOVERY_G = json.loads((GOLDEN / "recovery.json").read_text())
+
+
+def _entries():
+    return [StoreEntry(*e) for e in STORE["entries"]]
+
+
+# -- CRC ----------------------------------------------------------------------
+
+def test_crc32c_known_vectors():
+    assert crc32c(b"123456789") == 0xE3069283
+    assert crc32c(b"") == 0
+
+
+def test_crc32c_golden_vectors_and_chaining():
+    rng = np.random.default_rng(STORE["crc_seed"])
+    for v in STORE["crc_vectors"]:
+        b = rng.bytes(v["seed_len"])
+        assert hashlib.sha256(b).hexdigest() == v["sha"]
+        assert crc32c(b) == v["crc"]
+        k = len(b) // 3
+        assert crc32c(b[k:], crc32c(b[:k])) == v["crc"]
+
+
+def test_crc32c_many_and_combine_large():
+    from paper_2408_04307_b200 import device as D
+    rng = np.random.default_rng(3)
+    buf = rng.integers(0, 256, size=(200 << 20) + 12345, dtype=np.uint8)
+    offs = [0, 7, 1 << 20, (64 << 20) - 3, 5]
+    lens = [len(buf), (130 << 20) + 1, 0, 70 << 20, 1]
+    got = D.crc32c_many(buf, offs, lens, threads=4)
+    for o, n, c in zip(offs, lens, got):
+        assert int(c) == crc32c(buf[o:o + n])
+    a, b = buf[:1000].tobytes(), buf[1000:300000].tobytes()
+    assert D.crc32c_combine(crc32c(a), crc32c(b), len(b)) == crc32c(a + b)
+
+
+def test_oracle_crc_agrees_with_product_crc():
+    from oracle import pec_oracle as O
+    rng = np.random.default_rng(11)
+    for n in (0, 1, 15, 16, 17, 4095, 100001):
+        b = rng.bytes(n)
+        assert O.crc32c(b) == crc32c(b)
+        if n <= 2000:
+            assert O.crc32c_py(b) == crc32c(b)
+
+
+# -- store format ---------------------------------------------------------------
+
+def test_disk_layout_meta_and_manifest_are_byte_identical(tmp_path):
+    st = DiskStore(tmp_path)
+    st.write_version(3, iteration=17, checkpoint_index=2, entries=_entries())
+    vdir = tmp_path / "v000003"
+    assert (vdir / "meta.json").read_text() == STORE["meta_json"]
+    assert (vdir / "manifest.tsv").read_text() == STORE["manifest_tsv"]
+    files = sorted(str(p.relative_to(vdir)) for p in vdir.rglob("*") if p.is_file())
+    assert files == STORE["files"]
+    assert (vdir / "COMPLETE").stat().st_size == 0
+
+
+def test_real_payload_round_trip_and_flip_detection(tmp_path):
+    st = DiskStore(tmp_path, io_threads=4)
+    rng = np.random.default_rng(5)
+    ents = _entries()
+    pay = {e.store_key: rng.bytes(e.stop - e.start) for e in ents}
+    man = st.write_version(1, iteration=7, checkpoint_index=0, entries=ents, payloads=pay)
+    assert man.complete_marker
+    assert st.load_checkpoint(1) == pay
+    for k, (path, size, c) in st.manifest(1).entries.items():
+        assert size == len(pay[k]) and c == crc32c(pay[k])
+    # read_into places the bytes into a host buffer
+    buf = bytearray(1000)
+    st.read_into(1, {"neo.r1": (buf, 100)})
+    assert bytes(buf[100:164]) == pay["neo.r1"]
+    victim = tmp_path / "v000001" / "rank0000" / "neo.r0.bin"
+    data = bytearray(victim.read_bytes())
+    data[5] ^= 0xFF
+    victim.write_bytes(bytes(data))
+    with pytest.raises(ChecksumMismatchError) as exc:
+        st.load_checkpoint(1)
+    assert exc.value.key == "neo.r0"
+
+
+def test_split_write_then_publish_equals_single_writer(tmp_path):
+    a, b = DiskStore(tmp_path / "a"), DiskStore(tmp_path / "b")
+    ents = _entries()
+    a.write_version(4, 9, 1, ents)
+    rows = []
+    for rank in (0, 1):
+        rows += b.write_entries(4, 9, [e for e in ents if e.rank == rank])
+    b.publish(4, 9, 1, ents, rows)
+    for name in ("meta.json", "manifest.tsv"):
+        assert (tmp_path / "a/v000004" / name).read_bytes() == \
+            (tmp_path / "b/v000004" / name).read_bytes()
+
+
+def test_incomplete_version_ignored_and_crash_budget(tmp_path):
+    st = DiskStore(tmp_path)
+    st.write_version(1, 5, 0, _entries())
+    total = st.serialized_size(2, 9, 1, _entries())
+    with pytest.raises(CrashPoint):
+        st.write_version(2, 9, 1, _entries(), injector=TruncatingInjector(total // 2))
+    assert st.complete_versions() == [1]
+    with pytest.raises(IncompleteVersionError):
+        st.load_checkpoint(2)
+    st2 = DiskStore(tmp_path / "x")
+    total = st2.serialized_size(1, 5, 0, _entries())
+    st2.write_version(1, 5, 0, _entries(), injector=TruncatingInjector(total + 1))
+    assert st2.newest_complete() == 1
+    with pytest.raises(StoreError):
+        st2.write_version(1, 6, 1, _entries())
+
+
+def test_memory_store_parity(tmp_path):
+    disk, mem = DiskStore(tmp_path), MemoryStore()
+    for s in (disk, mem):
+        s.write_version(1, iteration=7, checkpoint_index=0, entries=_entries())
+    assert disk.load_checkpoint(1) == mem.load_checkpoint(1)
+    assert disk.manifest(1).entries == mem.manifest(1).entries
+    assert disk.meta(1).entries == mem.meta(1).entries
+    for k, v in mem.load_checkpoint(1).items():
+        assert v == entry_payload(k, 1, 7)
+
+
+# -- state machine ---------------------------------------------------------------
+
+def test_triple_buffer_transitions():
+    bufs = TripleBufferSet()
+    b1 = bufs.begin_snapshot(1, 10, 0, None, nodes=[0])
+    assert b1.status == SNAPSHOTTING
+    with pytest.raises(RuntimeError):
+        bufs.begin_snapshot(9, 99, 9, None, nodes=[0])
+    assert bufs.complete_snapshot(b1) is b1 and b1.status == PERSISTING
+    b2 = bufs.begin_snapshot(2, 20, 1, None, nodes=[0])
+    assert bufs.complete_snapshot(b2) is None and b2.status == SNAPSHOTTED
+    b3 = bufs.begin_snapshot(3, 30, 2, None, nodes=[0])
+    bufs.complete_snapshot(b3)
+    with pytest.raises(NoFreeBufferError):
+        bufs.begin_snapshot(4, 40, 3, None, nodes=[0])
+    assert bufs.complete_persist(b1) is b2 and b1.status == RECOVERY
+    with pytest.raises(NoFreeBufferError):
+        bufs.begin_snapshot(4, 40, 3, None, nodes=[0])
+    assert bufs.complete_persist(b2) is b3
+    assert b1.status == FREE and b1.content is None
+    assert bufs.begin_snapshot(4, 40, 3, None, nodes=[0]) is b1
+
+
+# -- recovery decisions vs reference -----------------------------------------------
+
+def _layout_from(case):
+    m = case["model"]
+    model = ModelSpec(**{**m, "non_expert_modules": tuple(map(tuple, m["non_expert_modules"]))})
+    gpn = case["gpus_per_node"]
+    cluster = ClusterSpec(num_nodes=case["dp"] // gpn, gpus_per_node=gpn, snapshot_bandwidth=1e9,
+                          persist_bandwidth=1e8, fb_time=0.01, update_time=0.002,
+                          restart_time=1.0)
+    return build_layout(model, ParallelSpec(case["dp"], case["ep"]), cluster)
+
+
+@pytest.mark.parametrize("i", range(len(RECOVERY_G["cases"])))
+def test_recovery_decisions_match_reference(i):
+    case = RECOVERY_G["cases"][i]
+    layout = _layout_from(case)
+    n = layout.model.experts_per_layer
+    pec = PecConfig(k_pec=case["k_snapshot"], k_snapshot=case["k_snapshot"],
+                    k_persist=case["k_persist"])
+    plan = plan_equal(layout, pec)
+    eng = CheckpointEngine(layout, MemoryStore())
+    kp = case["k_persist"]
+    for op in case["ops"]:
+        c = op["c"]
+        buf = eng.begin_snapshot(op["iteration"], c, plan.assignments[plan.phase_of(c)])
+        eng.complete_snapshot(buf)
+        if op["persisted"]:
+            sel = {m: select_window(c, m, n, kp, kp) for m in range(layout.model.num_moe_layers)}
+            eng.complete_persist(buf, eng.persist_entries(buf, sel))
+    want = case["result"]
+    if "error" in want:
+        with pytest.raises(Exception) as exc:
+            eng.resolve_recovery(set(case["failed"]), max_iteration=case["max_iteration"])
+        assert type(exc.value).__name__ == want["error"]
+        return
+    got = eng.resolve_recovery(set(case["failed"]), max_iteration=case["max_iteration"])
+    assert {k: list(v) for k, v in sorted(got.decisions.items())} == want["decisions"]
+    assert got.restart_iteration == want["restart_iteration"]
+    assert got.version_skew == want["version_skew"]
+
+
+def test_fig7_two_level_recovery():
+    layout = make_layout(n_experts=4, dp=4, ep=4, gpus_per_node=2, n_layers=1, epp=100)
+    pec = PecConfig(k_pec=2, k_snapshot=2, k_persist=1)
+    plan = plan_equal(layout, pec)
+    eng = CheckpointEngine(layout, MemoryStore())
+    for c, it in enumerate((10, 20, 30)):
+        buf = eng.begin_snapshot(it, c, plan.assignments[plan.phase_of(c)])
+        eng.complete_snapshot(buf)
+        sel = {0: select_window(c, 0, 4, 1, 1)}
+        eng.complete_persist(buf, eng.persist_entries(buf, sel))
+    d = eng.resolve_recovery({0}).decisions
+    assert d["ew.L0.E0"][:1] == ("storage",) and d["ew.L0.E0"].restored_iteration == 10
+    assert d["ew.L0.E2"].source == "memory" and d["ew.L0.E2"].node == 1
+    assert d["ew.L0.E3"].source == "memory" and d["ew.L0.E3"].restored_iteration == 30
+    d1 = eng.resolve_recovery({1}).decisions
+    assert d1["ew.L0.E3"].source == "initial"
+    with pytest.raises(UnrecoverableStateError):
+        CheckpointEngine(layout, MemoryStore()).resolve_recovery(set())
