@@ -243,62 +243,70 @@ def run_reference(args):
 
 
 def run_b200(args):
+    import shutil
+    import tempfile
     import torch
     rank, local, world = dist_init(args.gpus)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2408_04307_b200 import device as D
     from paper_2408_04307_b200.arena import StateArena
-    from paper_2408_04307_b200.staging import DeviceTable, StagingLayout
+    from paper_2408_04307_b200.counting import DeviceTokenCounters
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore
 
     w, layout, plan = build_workload(args, rank)
     t_fill = time.time()
     arena = StateArena(layout, ranks=[rank], device=dev, expert_tensors=w.expert_tensors)
     torch.cuda.synchronize()
     t_fill = time.time() - t_fill
-    layouts = [StagingLayout.build(plan.assignments[p][rank], arena, rank)
-               for p in range(plan.period)]
-    stage_bytes = max(s.nbytes for s in layouts)
-    staging = torch.empty(stage_bytes, dtype=torch.uint8, device=dev)
+    L, E, top_k = layout.model.num_moe_layers, layout.model.experts_per_layer, layout.model.top_k
+    routed = w.tokens_per_rank * top_k
+    counters = DeviceTokenCounters(L, E, dev, DeviceTokenCounters.capacity_for(
+        w.capacity_factor, [routed] * L, E))
+    persist = args.persist if args.persist != "auto" else ("shm" if world == 1 else "none")
+    store_root = None
+    store = None
+    if persist != "none":
+        base = "/dev/shm" if persist == "shm" else tempfile.gettempdir()
+        store_root = tempfile.mkdtemp(prefix="pec_bench_", dir=base)
+        store = DiskStore(store_root, io_threads=8)
+    control = None
+    if world > 1 and store is not None:
+        import torch.distributed as dist
+        control = dist.new_group(backend="gloo")
     mode = {"vec": D.MODE_VEC, "bulk": D.MODE_BULK}[args.engine]
-    tables = []
-    for s in layouts:
-        t, total = s.descriptors(arena.base_address, staging.data_ptr(),
-                                 chunk_log2=args.chunk_log2)
-        tables.append(DeviceTable(t, total, dev, args.chunk_log2))
-    L, E = layout.model.num_moe_layers, layout.model.experts_per_layer
+    ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=1, ranks=[rank],
+                         counters=counters, control_group=control, pack_mode=mode,
+                         chunk_log2=args.chunk_log2)
+    eng = ck.engine
+    eng._ensure_staging(ck.max_snapshot_bytes())
     k_s = w.pec.k_snapshot
     sel = torch.empty((L, min(k_s, E)), dtype=torch.int32, device=dev)
-    stream = torch.cuda.Stream(device=dev)
+    stream = eng.pack_stream
 
-    def step(c, ev_pair=None):
+    def step(c):
+        """select (device) + pack of checkpoint c; returns (t0, t1, bytes)."""
         p = plan.phase_of(c)
-        with torch.cuda.stream(stream):
-            D.select_sequential(c, L, E, k_s, w.pec.k_persist, sel, stream=stream)
-            if ev_pair is not None:
-                ev_pair[0].record(stream)
-            tab = tables[p]
-            D.pack(tab.tensor, tab.n, tab.total_chunks, tab.chunk_log2, mode, stream=stream)
-            if ev_pair is not None:
-                ev_pair[1].record(stream)
-        return layouts[p].payload_bytes
+        D.select_sequential(c, L, E, k_s, w.pec.k_persist, sel, stream=stream)
+        return eng.pack_only(plan.assignments[p], plan_key=("phase", p), stream=stream)
 
-    # warm-up
     for c in range(args.warmup):
         step(c)
     stream.synchronize()
     barrier(world)
     torch.cuda.synchronize()
 
-    # ---- timed device region --------------------------------------------
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    # ---- timed device region: inputs resident in HBM ------------------------
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = []
     moved = 0
     with ClockSampler(local) as clk:
         t0.record(stream)
         for k in range(args.steps):
-            moved += step(args.warmup + k, evs[k])
+            a, b, n = step(args.warmup + k)
+            evs.append((a, b))
+            moved += n
         t1.record(stream)
         stream.synchronize()
     torch.cuda.synchronize()
@@ -309,7 +317,6 @@ def run_b200(args):
     total_moved = sum_over_ranks(moved, world, dev)
     value = total_moved / (max_ms / 1e3) / 1e9
 
-    # roofline of the dominant kernel (pack): 2*S_rank bytes per launch
     hbm_peak, peak_kind = measured_peaks()
     avg_pack_ms = statistics.mean(pack_ms)
     achieved = 2 * (moved / args.steps) / (avg_pack_ms / 1e3) / 1e9
@@ -321,42 +328,64 @@ def run_b200(args):
         except Exception:
             traffic = None
 
-    # ---- e2e: pack + drain into pinned host memory -----------------------
+    # ---- e2e through the public API: router ids H2D -> count -> select ->
+    #      pack -> drain into pinned host memory (SNAPSHOTTED) -> host read;
+    #      the persist of each version runs behind on the persist thread
     e2e = None
+    persist_info = None
     if not args.no_e2e:
-        host = torch.empty(stage_bytes, dtype=torch.uint8, pin_memory=True)
-        copy_stream = torch.cuda.Stream(device=dev)
-        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        e2e_steps = max(1, min(args.e2e_steps, 2))  # <= 2 so no buffer waits on persist
+        rng = np.random.default_rng(1234 + rank)
+        ids_host = [torch.from_numpy(rng.integers(0, E, size=(L, routed), dtype=np.int32)).pin_memory()
+                    for _ in range(e2e_steps + 1)]
+        ids_dev = torch.empty((L, routed), dtype=torch.int32, device=dev)
+        # warm the host path once (pinned-page first touch, table caches)
+        for b in range(len(eng.host)):
+            eng._ensure_host(b, eng.staging.numel())
+        warm = torch.empty(min(eng.staging.numel(), 1 << 30), dtype=torch.uint8, pin_memory=True)
+        warm.copy_(eng.staging[:warm.numel()])
+        del warm
         barrier(world)
         torch.cuda.synchronize()
-        d2h = 0
+        h2d = d2h = 0
+        base_it = args.warmup + args.steps + 10
         tw = time.perf_counter()
         for k in range(e2e_steps):
-            c = args.warmup + args.steps + k
-            n = step(c)
-            p = plan.phase_of(c)
-            done = torch.cuda.Event()
-            done.record(stream)
-            copy_stream.wait_event(done)
-            with torch.cuda.stream(copy_stream):
-                host[:layouts[p].nbytes].copy_(staging[:layouts[p].nbytes], non_blocking=True)
-            copy_stream.synchronize()
-            # host read of the step result: checksum of the first entry's first bytes
-            _ = int(host[: min(64, layouts[p].nbytes)].sum())
-            d2h += layouts[p].nbytes
+            it = base_it + k
+            ids_dev.copy_(ids_host[k], non_blocking=True)
+            h2d += ids_host[k].numel() * 4
+            counters.add_iteration(ids_dev)
+            buf = ck.checkpoint(it)               # select + plan + pack + drain
+            ck._complete(buf)                     # wait for SNAPSHOTTED
+            rec = eng._inflight[buf.buffer_id]
+            first = rec.layouts[rank].entries[0]
+            _ = int(eng.entry_view(buf, rank, first.store_key)[0])  # host read
+            d2h += rec.nbytes
         e2e_s = time.perf_counter() - tw
         e2e_s = max_over_ranks(e2e_s, world, dev)
-        e2e_moved = sum_over_ranks(sum(layouts[plan.phase_of(args.warmup + args.steps + k)].payload_bytes
-                                       for k in range(e2e_steps)), world, dev)
+        e2e_moved = sum_over_ranks(sum(eng.stats["snap_bytes"][-e2e_steps:]), world, dev)
         e2e = {"value": round(e2e_moved / e2e_s / 1e9, 3), "unit": UNIT,
-               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h // e2e_steps,
-               "steps": e2e_steps, "ms_per_step": round(e2e_s / e2e_steps * 1e3, 3)}
+               "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
+               "steps": e2e_steps, "ms_per_step": round(e2e_s / e2e_steps * 1e3, 2),
+               "drain_ms": [round(x, 2) for x in eng.stats["drain_ms"][-e2e_steps:]],
+               "what": "router-id H2D + count + select + pack + D2H drain to pinned host"}
+        tp0 = time.perf_counter()
+        ck.finish()
+        if store is not None and eng.stats["persist_s"]:
+            persisted = sum(eng.stats["snap_bytes"][-e2e_steps:])
+            persist_info = {"target": persist, "versions": len(eng.stats["persist_s"]),
+                            "seconds": [round(x, 2) for x in eng.stats["persist_s"]],
+                            "GBps": round(persisted / max(sum(eng.stats["persist_s"]), 1e-9) / 1e9, 2)}
+    ck.close()
+    if store_root:
+        shutil.rmtree(store_root, ignore_errors=True)
 
     # ---- CPU baseline (rank 0, N == 1 only) ----------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
-        gbs, desc = cpu_pack_sample(layouts[0].entries, int(args.cpu_sample_gb * 1e9), threads,
+        first_layout = eng._table_for(plan.assignments[0], ("phase", 0))[1][rank]
+        gbs, desc = cpu_pack_sample(first_layout.entries, int(args.cpu_sample_gb * 1e9), threads,
                                     args.cpu_seconds)
         cpu = {"value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",
                "sample": desc}
@@ -372,7 +401,7 @@ def run_b200(args):
                        "bytes_per_step_rank0": moved // args.steps,
                        "state_resident_gb": round(arena.resident_bytes() / 1e9, 2),
                        "engine": args.engine, "chunk_log2": args.chunk_log2,
-                       "l2": "inputs (>= 9.9 GB per step) exceed the 126 MB L2",
+                       "l2": "no flush needed: each step reads >= 9.9 GB (> 126 MB L2)",
                        "parallelism": f"dp{layout.n_ranks}-ep{layout.parallel.ep_degree}"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
@@ -380,11 +409,21 @@ def run_b200(args):
                          "kernel": f"pec_pack ({args.engine})",
                          "avg_launch_ms": round(avg_pack_ms, 4)},
             "e2e": e2e,
+            "host_link": ({"achieved": round(statistics.mean(
+                              [d / (m / 1e3) / 1e9 for d, m in zip(
+                                  [e2e["d2h_bytes_per_step"]] * len(e2e["drain_ms"]),
+                                  e2e["drain_ms"])]), 2),
+                           "peak": args.d2h_peak, "unit": "GB/s",
+                           "peak_kind": "measured pinned D2H (tools/d2h_probe.py)"}
+                          if e2e else None),
+            "persist": persist_info,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": 2 * args.steps,
             "fill_s": round(t_fill, 2),
         }
+        if line["host_link"]:
+            line["host_link"]["frac"] = round(line["host_link"]["achieved"] / args.d2h_peak, 4)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -399,9 +438,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="mixtral", choices=["toy", "gpt125m", "gpt350m", "mixtral"])
-    ap.add_argument("--engine", default="vec", choices=["vec", "bulk"])
+    ap.add_argument("--engine", default="bulk", choices=["vec", "bulk"])
     ap.add_argument("--chunk-log2", type=int, default=15)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--persist", default="auto", choices=["auto", "none", "shm", "disk"])
+    ap.add_argument("--d2h-peak", type=float, default=56.8,
+                    help="measured pinned D2H GB/s of this pool's B200 host link")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-gb", type=float, default=2.0)

@@ -481,30 +481,55 @@ copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total, int
   }
 }
 
+// Per-device launch geometry, computed once (attribute setting and
+// occupancy queries are host round trips that would otherwise sit between
+// the caller's start event and the kernel).
+struct CopyGeometry {
+  int ready = 0;
+  int vec_grid = 0;
+  int bulk_grid = 0;
+  int bulk_smem = 0;
+};
+
+int copy_geometry(CopyGeometry** out) {
+  static CopyGeometry geo[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return PEC_E_CUDA;
+  CopyGeometry& g = geo[dev];
+  if (!g.ready) {
+    const int sms = sm_count();
+    g.bulk_smem = kBulkStages << kStageLog2;
+    if (cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             g.bulk_smem) != cudaSuccess)
+      return PEC_E_CUDA;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_bulk_kernel, kBulkThreads, g.bulk_smem);
+    g.bulk_grid = sms * (per_sm < 1 ? 1 : per_sm);
+    per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_vec_kernel, kVecThreads, 0);
+    g.vec_grid = sms * (per_sm < 1 ? 1 : per_sm);
+    g.ready = 1;
+  }
+  *out = &g;
+  return PEC_OK;
+}
+
 int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, int lg, int mode, void* stream) {
   if (n < 0 || lg < 12 || lg > 24) return PEC_E_INVAL;
+  if (mode < 0 || mode > 2) return PEC_E_INVAL;
   if (total == 0 || n == 0) return PEC_OK;
   if (descs == nullptr) return PEC_E_INVAL;
-  if (mode < 0 || mode > 2) return PEC_E_INVAL;
-  const int sms = sm_count();
+  CopyGeometry* g = nullptr;
+  const int rc = copy_geometry(&g);
+  if (rc != PEC_OK) return rc;
   cudaStream_t st = as_stream(stream);
   if (mode == 2) {
     const int smem = kBulkStages << (lg < kStageLog2 ? lg : kStageLog2);
-    if (cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return PEC_E_CUDA;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_bulk_kernel, kBulkThreads, smem);
-    if (per_sm < 1) per_sm = 1;
-    uint64_t grid = (uint64_t)sms * per_sm;
-    if (grid > total) grid = total;
+    const uint64_t grid = (uint64_t)g->bulk_grid < total ? (uint64_t)g->bulk_grid : total;
     copy_bulk_kernel<<<(unsigned)grid, kBulkThreads, smem, st>>>(descs, n, total, lg);
     return launch_status();
   }
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_vec_kernel, kVecThreads, 0);
-  if (per_sm < 1) per_sm = 1;
-  uint64_t grid = (uint64_t)sms * per_sm;
-  if (grid > total) grid = total;
+  const uint64_t grid = (uint64_t)g->vec_grid < total ? (uint64_t)g->vec_grid : total;
   copy_vec_kernel<<<(unsigned)grid, kVecThreads, 0, st>>>(descs, n, total, lg);
   return launch_status();
 }
@@ -575,12 +600,12 @@ int pec_select_load_aware(int64_t* counters, int L, int E, int K,
 
 int pec_pack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
              int chunk_log2, int mode, void* stream) {
-  return launch_copy(descs, n, total_chunks, chunk_log2, mode == 0 ? 1 : mode, stream);
+  return launch_copy(descs, n, total_chunks, chunk_log2, mode == 0 ? 2 : mode, stream);
 }
 
 int pec_unpack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
                int chunk_log2, int mode, void* stream) {
-  return launch_copy(descs, n, total_chunks, chunk_log2, mode == 0 ? 1 : mode, stream);
+  return launch_copy(descs, n, total_chunks, chunk_log2, mode == 0 ? 2 : mode, stream);
 }
 
 int64_t pec_plan_chunks(pec_copy_desc* host_descs, int n, int chunk_log2) {

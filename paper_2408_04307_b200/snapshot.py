@@ -144,6 +144,22 @@ class DeviceCheckpointEngine(CheckpointEngine):
         return entry
 
     # -- snapshot --------------------------------------------------------------------
+    def pack_only(self, assignment: PhaseAssignment, plan_key=None, stream=None):
+        """Pack the local ranks' ranges into HBM staging without draining
+        (the consistency-critical device step alone).  Returns
+        (start_event, end_event, payload_bytes)."""
+        import torch
+        table, layouts, region, nbytes = self._table_for(assignment, plan_key)
+        s = stream or self.pack_stream
+        if self._staging_free is not None:
+            s.wait_event(self._staging_free)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(s)
+        D.pack(table.tensor, table.n, table.total_chunks, table.chunk_log2, self.pack_mode,
+               stream=s)
+        t1.record(s)
+        return t0, t1, sum(l.payload_bytes for l in layouts.values())
+
     def begin_snapshot(self, iteration: int, checkpoint_index: int,
                        assignment: PhaseAssignment, plan_key=None, compute_stream=None) -> Buffer:
         import torch
@@ -399,6 +415,13 @@ class PecCheckpointer:
             self._start_persist(promoted)
 
     def _start_persist(self, buf: Buffer) -> None:
+        if self.engine.store is None:
+            # snapshot tier only (no persist tier configured): the buffer is
+            # published to the in-memory recovery role without any writes
+            nxt = self.engine.buffers.complete_persist(buf)
+            if nxt is not None:
+                self._start_persist(nxt)
+            return
         entries = self.engine.persist_entries(buf, self.persist_sel[buf.version])
         if self.async_persist:
             self.engine.start_persist(buf, entries)
