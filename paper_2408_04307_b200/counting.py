@@ -64,22 +64,23 @@ class DeviceTokenCounters:
                ) -> Tuple["object", "object"]:
         """Two-tier load-aware selection on device: snapshot set from the
         snapshot tier, persist set restricted to it from the persist tier,
-        both tiers' selected counters reset.  Returns device int32
+        both tiers' selected counters reset.  With a process group the
+        selection runs on the all-reduced global counts
+        (`distributed.global_two_tier_select`).  Returns device int32
         [L, k_s] / [L, k_p] (ids ascending per layer)."""
         import torch
-        import torch.distributed as dist
+        from .distributed import _world, global_two_tier_select
         L = self.n_layers
-        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
-        src = self.all_reduced(group) if multi else self.counts
-        snap = torch.empty((L, k_snapshot), dtype=torch.int32, device=self.device)
-        pers = torch.empty((L, k_persist), dtype=torch.int32, device=self.device)
-        D.select_load_aware(src[SNAPSHOT_TIER], k_snapshot, snap, zero_selected=True, stream=stream)
-        D.select_load_aware(src[PERSIST_TIER], k_persist, pers, pool=snap, zero_selected=True,
-                            stream=stream)
-        if multi:
-            # zero the same entries in the local counters
-            self.counts[SNAPSHOT_TIER].scatter_(1, snap.long().clamp_min(0), 0)
-            self.counts[PERSIST_TIER].scatter_(1, pers.long().clamp_min(0), 0)
+
+        def kernel(counts2d, k, pool, zero=False):
+            out = torch.empty((L, k), dtype=torch.int32, device=self.device)
+            D.select_load_aware(counts2d, k, out, pool=pool, zero_selected=zero, stream=stream)
+            return out
+
+        if _world(group) > 1:
+            return global_two_tier_select(self.counts, k_snapshot, k_persist, kernel, group)
+        snap = kernel(self.counts[SNAPSHOT_TIER], k_snapshot, None, zero=True)
+        pers = kernel(self.counts[PERSIST_TIER], k_persist, snap, zero=True)
         return snap, pers
 
     def reset_to(self, snapshot_tier, persist_tier) -> None:

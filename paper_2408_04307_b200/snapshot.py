@@ -234,25 +234,13 @@ class DeviceCheckpointEngine(CheckpointEngine):
 
     # -- persist --------------------------------------------------------------------------
     def _write(self, buf: Buffer, entries: List[StoreEntry]) -> float:
-        """Write this process's entry files; multi-process: gather rows, rank
-        0 publishes (single-writer-identical files), everyone syncs."""
+        """Write this process's entry files and publish the version
+        (multi-process: `distributed.commit_version`)."""
+        from .distributed import commit_version
         t0 = time.perf_counter()
         local = [e for e in entries if e.rank in self.ranks]
-        pay = self.payloads(buf, local)
-        version, it, c = buf.version, buf.iteration, buf.checkpoint_index
-        if self.group is None:
-            self.store.check_version(version)
-            rows = self.store.write_entries(version, it, local, payloads=pay)
-            self.store.publish(version, it, c, entries, rows)
-        else:
-            import torch.distributed as dist
-            rows = self.store.write_entries(version, it, local, payloads=pay)
-            gathered = [None] * dist.get_world_size(self.group)
-            dist.all_gather_object(gathered, rows, group=self.group)
-            if dist.get_rank(self.group) == 0:
-                all_rows = [r for part in gathered for r in part]
-                self.store.publish(version, it, c, entries, all_rows)
-            dist.barrier(group=self.group)
+        commit_version(self.store, buf.version, buf.iteration, buf.checkpoint_index, entries,
+                       self.ranks, self.payloads(buf, local), group=self.group)
         return time.perf_counter() - t0
 
     def start_persist(self, buf: Buffer, entries: List[StoreEntry]) -> Future:

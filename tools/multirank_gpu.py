@@ -1,0 +1,133 @@
+"""Multi-GPU check of the PEC path (run under torchrun, one process per GPU).
+
+GPT-MoE 350M-16E, dp=ep=N deployment (N = world size), K_pec=2 load-aware
+(equal_pec), one rank per process.  Per checkpoint:
+  * every rank counts its own router ids (different seeds) on device,
+  * NCCL all-reduce of the [2, L, E] counters -> identical global selection
+    on every rank == the oracle's selection on the summed counts,
+  * pack + drain + multi-writer persist (gloo control group) to a shared store,
+  * every rank verifies its persisted entries against its arena bytes,
+then a storage restore of every rank's units after wiping them is checked
+bit-exact.  Prints one JSON line per rank; exits non-zero on any mismatch.
+"""
+
+import json
+import os
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+    from oracle import pec_oracle as O
+    from paper_2408_04307_b200 import PecConfig, configs
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.counting import DeviceTokenCounters
+    from paper_2408_04307_b200.restore import restore
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore
+
+    rank, local, world = (int(os.environ[k]) for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    control = dist.new_group(backend="gloo")
+    root = os.environ.get("PEC_STORE", "/dev/shm/pec_multirank")
+    if rank == 0:
+        import shutil
+        shutil.rmtree(root, ignore_errors=True)
+    dist.barrier()
+
+    w = configs.gpt350m_16e(k_pec=2, strategy="equal_pec", dp=world, ep=world)
+    layout = w.layout()
+    L, E = layout.model.num_moe_layers, layout.model.experts_per_layer
+    arena = StateArena(layout, [rank], dev, w.expert_tensors)
+    routed = 4096 * 2
+    cap = DeviceTokenCounters.capacity_for(1.25, [routed] * L, E)
+    counters = DeviceTokenCounters(L, E, dev, cap)
+    pec = PecConfig(k_pec=2, selection="load_aware", k_snapshot=2, k_persist=1)
+    store = DiskStore(root)
+    ck = PecCheckpointer(layout, arena, store, pec, "equal_pec", i_ckpt=3, ranks=[rank],
+                         counters=counters, group=None, control_group=control,
+                         async_persist=False)
+    ck.group = dist.group.WORLD  # NCCL group for the counter all-reduce
+
+    glob = np.zeros((2, L, E), dtype=np.int64)
+    ok = True
+    persisted_bytes = {}
+    t0 = time.time()
+    for it in range(1, 10):
+        ids = {r: np.stack([O.zipf_router_ids(100 + r, it, m, E, routed, 1.1) for m in range(L)])
+               for r in range(world)}
+        for r in range(world):
+            c = O.route_counts(ids[r], E, cap)
+            glob[0] += c
+            glob[1] += c
+        buf = ck.step(it, torch.from_numpy(ids[rank]).to(dev))
+        if buf is not None:
+            ss, ps, glob[0], glob[1] = O.two_tier_load_aware(glob[0], glob[1], 2, 1)
+            got_p = [sorted(ck.persist_sel[buf.version][m]) for m in range(L)]
+            ok &= got_p == ps
+            # snapshot set: experts appearing in the phase assignment (any rank)
+            snap = {m: set() for m in range(L)}
+            for rr, ranges in buf.content.items():
+                for a in ranges:
+                    u = layout.by_key[a.key]
+                    if u.layer is not None:
+                        snap[u.layer].add(u.expert)
+            ok &= [sorted(snap[m]) for m in range(L)] == ss
+            torch.cuda.synchronize()
+            persisted_bytes[buf.version] = arena.buffer.cpu().numpy().copy()
+            ck.wait_pack()
+    ck.finish()
+    sel_ok = ok
+    # verify persisted entries of this rank against the arena at snapshot time
+    versions = store.complete_versions()
+    files_ok = bool(versions)
+    for v in versions:
+        meta = store.meta(v)
+        mine = [k for k, e in meta.entries.items() if e.rank == rank]
+        data = store.load_checkpoint(v, mine)
+        snapimg = persisted_bytes[v]
+        for k in mine:
+            e = meta.entries[k]
+            off = arena.slot(e.unit_key).offset + e.start
+            files_ok &= data[k] == bytes(snapimg[off:off + e.stop - e.start])
+    dist.barrier()
+    # storage restore of this rank's resident units that the newest version covers
+    plan = ck.engine.resolve_recovery({0}, max_iteration=None)  # node 0 (all ranks) failed
+    ck.engine.on_fault({0})
+    keys = [k for k, d in plan.decisions.items() if arena.has(k) and d.source == "storage"]
+    before = arena.buffer.cpu().numpy().copy()
+    for k in keys:
+        arena.unit_bytes(k).zero_()
+    rep = restore(ck.engine, plan, keys=keys)
+    after = arena.buffer.cpu().numpy()
+    restore_ok = True
+    for k in keys:
+        d = plan.decisions[k]
+        s = arena.slot(k)
+        restore_ok &= np.array_equal(after[s.offset:s.offset + s.size],
+                                     persisted_bytes[d.version][s.offset:s.offset + s.size])
+    ck.close()
+    res = {"rank": rank, "world": world, "selection_ok": bool(sel_ok), "files_ok": bool(files_ok),
+           "restore_ok": bool(restore_ok), "versions": versions, "restored_units": len(keys),
+           "restored_bytes": rep.storage_bytes, "seconds": round(time.time() - t0, 1)}
+    print(json.dumps(res), flush=True)
+    dist.barrier()
+    if rank == 0:
+        import shutil
+        shutil.rmtree(root, ignore_errors=True)
+    dist.destroy_process_group()
+    return 0 if (sel_ok and files_ok and restore_ok) else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
