@@ -112,7 +112,8 @@ def dist_init(n_gpus):
     rank, local, world = env_rank()
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=None)
+        import torch
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, local, world
 
 
@@ -178,6 +179,71 @@ def cpu_pack_sample(entries, sample_bytes: int, threads: int, min_seconds: float
     desc = (f"oracle numpy pack of the first {payload / 1e9:.2f} GB of rank ranges "
             f"({len(copies)} entries) x{reps} passes, {threads} threads")
     return payload * reps / dt / 1e9, desc
+
+
+# ---------------------------------------------------------------------------
+# exposed checkpoint stall: synthetic training loop with and without PEC
+# ---------------------------------------------------------------------------
+
+def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float):
+    """Synthetic per-rank training loop on the compute stream: an F&B proxy
+    (bf16 8192^3 GEMMs, calibrated to ~fb_ms) then an update proxy (one
+    in-place pass over the whole state arena: HBM-bound like a fused Adam
+    step over the rank's ~85 GB shard).  With checkpointing, every i_ckpt-th
+    iteration calls PecCheckpointer.checkpoint after its update (the pack
+    photographs the updated state on the side stream, overlapping the next
+    F&B) and every update first waits for the pending pack.  Returns the
+    device time per iteration with/without and the difference."""
+    import torch
+    a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    b = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    c = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
+    words = arena.buffer.view(torch.int32)
+    compute = torch.cuda.current_stream(dev)
+    for _ in range(3):
+        torch.matmul(a, b, out=c)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        torch.matmul(a, b, out=c)
+    e1.record()
+    e1.synchronize()
+    gemm_ms = e0.elapsed_time(e1) / 10
+    n_gemm = max(1, int(round(fb_ms / gemm_ms)))
+    e0.record()
+    words.add_(1)
+    e1.record()
+    e1.synchronize()
+    update_ms = e0.elapsed_time(e1)
+
+    def run(with_ckpt: bool, base_it: int) -> float:
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(compute)
+        for k in range(1, iters + 1):
+            it = base_it + k
+            for _ in range(n_gemm):                 # forward + backward
+                torch.matmul(a, b, out=c)
+            if with_ckpt:
+                ck.poll()
+                ck.wait_pack(stream=compute)        # the update may not race the pack
+            words.add_(1)                           # optimizer step
+            if with_ckpt and it % i_ckpt == 0:
+                ck.checkpoint(it)                   # select + plan + pack + drain
+        t1.record(compute)
+        t1.synchronize()
+        return t0.elapsed_time(t1) / iters
+
+    run(False, 0)  # warm
+    without = run(False, 0)
+    with_ = run(True, 10 ** 6)
+    ck.finish()
+    return {"i_ckpt": i_ckpt, "iters": iters, "checkpoints": iters // i_ckpt,
+            "fb_ms": round(n_gemm * gemm_ms, 1), "fb_gemms": n_gemm,
+            "update_ms": round(update_ms, 2),
+            "iter_ms_without": round(without, 3), "iter_ms_with": round(with_, 3),
+            "exposed_ms_per_iter": round(with_ - without, 3),
+            "overhead_frac": round((with_ - without) / without, 5)}
 
 
 # ---------------------------------------------------------------------------
@@ -333,15 +399,21 @@ def run_b200(args):
     #      the persist of each version runs behind on the persist thread
     e2e = None
     persist_info = None
+    pin_s = 0.0
+    if not (args.no_e2e and args.no_stall):
+        # pin the host snapshot buffers once, before any timing (cudaHostAlloc
+        # pins ~2 GB/s; a training job does this at start-up): 3 with a
+        # persist tier, 2 without (buffers then recycle through RECOVERY)
+        tpin = time.perf_counter()
+        for b in range(3 if store is not None else 2):
+            eng._ensure_host(b, eng.staging.numel())
+        pin_s = time.perf_counter() - tpin
     if not args.no_e2e:
         e2e_steps = max(1, min(args.e2e_steps, 2))  # <= 2 so no buffer waits on persist
         rng = np.random.default_rng(1234 + rank)
         ids_host = [torch.from_numpy(rng.integers(0, E, size=(L, routed), dtype=np.int32)).pin_memory()
                     for _ in range(e2e_steps + 1)]
         ids_dev = torch.empty((L, routed), dtype=torch.int32, device=dev)
-        # warm the host path once (pinned-page first touch, table caches)
-        for b in range(e2e_steps):  # only the buffers the e2e steps use
-            eng._ensure_host(b, eng.staging.numel())
         warm = torch.empty(min(eng.staging.numel(), 1 << 30), dtype=torch.uint8, pin_memory=True)
         warm.copy_(eng.staging[:warm.numel()])
         del warm
@@ -349,6 +421,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         h2d = d2h = 0
         base_it = args.warmup + args.steps + 10
+        ck.hold_persist(True)   # measure the snapshot tier alone; persist after
         tw = time.perf_counter()
         for k in range(e2e_steps):
             it = base_it + k
@@ -368,7 +441,8 @@ def run_b200(args):
                "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                "steps": e2e_steps, "ms_per_step": round(e2e_s / e2e_steps * 1e3, 2),
                "drain_ms": [round(x, 2) for x in eng.stats["drain_ms"][-e2e_steps:]],
-               "what": "router-id H2D + count + select + pack + D2H drain to pinned host"}
+               "what": "router-id H2D + count + select + pack + D2H drain to pinned host",
+               "host_pin_s": round(pin_s, 1)}
         tp0 = time.perf_counter()
         ck.finish()
         if store is not None and eng.stats["persist_s"]:
@@ -376,6 +450,11 @@ def run_b200(args):
             persist_info = {"target": persist, "versions": len(eng.stats["persist_s"]),
                             "seconds": [round(x, 2) for x in eng.stats["persist_s"]],
                             "GBps": round(persisted / max(sum(eng.stats["persist_s"]), 1e-9) / 1e9, 2)}
+    stall = None
+    if not args.no_stall:
+        stall = measure_stall(ck, arena, dev, args.stall_iters, args.i_ckpt, args.fb_ms)
+        stall["exposed_ms_per_iter"] = round(max_over_ranks(stall["exposed_ms_per_iter"],
+                                                            world, dev), 3)
     ck.close()
     if store_root:
         shutil.rmtree(store_root, ignore_errors=True)
@@ -417,6 +496,7 @@ def run_b200(args):
                            "peak_kind": "measured pinned D2H (tools/d2h_probe.py)"}
                           if e2e else None),
             "persist": persist_info,
+            "stall": stall,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": 2 * args.steps,
@@ -446,6 +526,10 @@ def main():
                     help="measured pinned D2H GB/s of this pool's B200 host link")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-stall", action="store_true")
+    ap.add_argument("--stall-iters", type=int, default=20)
+    ap.add_argument("--i-ckpt", type=int, default=10)
+    ap.add_argument("--fb-ms", type=float, default=100.0)
     ap.add_argument("--cpu-sample-gb", type=float, default=2.0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

@@ -402,7 +402,19 @@ class PecCheckpointer:
         if promoted is not None:
             self._start_persist(promoted)
 
+    def hold_persist(self, hold: bool = True) -> None:
+        """Pause (hold=True) or resume the persist tier.  While held,
+        snapshots still complete (SNAPSHOTTED) and queue for persist; on
+        resume the oldest queued one starts."""
+        self._persist_held = hold
+        if not hold:
+            p = self.engine.buffers.persisting
+            if p is not None and p.buffer_id not in self.engine._persist:
+                self._start_persist(p)
+
     def _start_persist(self, buf: Buffer) -> None:
+        if getattr(self, "_persist_held", False):
+            return  # stays PERSISTING (queued) until hold_persist(False)
         if self.engine.store is None:
             # snapshot tier only (no persist tier configured): the buffer is
             # published to the in-memory recovery role without any writes
@@ -422,6 +434,11 @@ class PecCheckpointer:
         p = self.engine.buffers.persisting
         if p is None:
             return False
+        if p.buffer_id not in self.engine._persist:
+            # queued behind hold_persist: the caller needs the buffer now
+            self._persist_held = False
+            self._start_persist(p)
+            return True
         nxt = self.engine.finish_persist(p)
         if nxt is not None:
             self._start_persist(nxt)
@@ -440,6 +457,8 @@ class PecCheckpointer:
 
     def finish(self) -> None:
         """Drain all in-flight snapshot and persist work."""
+        if getattr(self, "_persist_held", False):
+            self.hold_persist(False)
         snapping = self.engine.buffers.snapshotting
         if snapping is not None:
             self._complete(snapping)
