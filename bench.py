@@ -253,7 +253,9 @@ def build_workload(args, rank):
     from paper_2408_04307_b200.planner import plan_adaptive, plan_equal
     w = configs.WORKLOADS[args.workload]()
     layout = w.layout()
-    if w.strategy == "adaptive_pec":
+    if w.pec.selection == "load_aware":
+        plan = None  # assignments are built per checkpoint (on device)
+    elif w.strategy == "adaptive_pec":
         plan = plan_adaptive(layout, w.pec)
     else:
         plan = plan_equal(layout, w.pec)
@@ -285,7 +287,16 @@ def run_reference(args):
             s.offset = self.o[key]
             return s
 
-    st = StagingLayout.build(plan.assignments[0][0], _Slots(), 0)
+    if plan is not None:
+        ranges0 = plan.assignments[0][0]
+    else:  # load-aware: a representative due set of the same size (window c=0)
+        from paper_2408_04307_b200.planner import build_phase_assignment
+        from paper_2408_04307_b200.selector import select_window
+        n = layout.model.experts_per_layer
+        due = {m: select_window(0, m, n, w.pec.k_snapshot, w.pec.k_persist)
+               for m in range(layout.model.num_moe_layers)}
+        ranges0 = build_phase_assignment(layout, due, w.strategy)[0]
+    st = StagingLayout.build(ranges0, _Slots(), 0)
     sample = min(args.cpu_sample_gb, st.payload_bytes / 1e9)
     per_step = []
     for i in range(args.warmup + args.steps):
@@ -298,7 +309,7 @@ def run_reference(args):
             "ms_per_step": round(sample * 1e9 / (value * 1e9) * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": w.name, "rank": 0, "plan": plan.strategy,
+            "config": {"workload": w.name, "rank": 0, "plan": w.strategy,
                        "k_pec": w.pec.k_pec, "sample_gb": round(sample, 3)},
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads,
                              "kind": "port", "sample": desc},
@@ -319,6 +330,7 @@ def run_b200(args):
     from paper_2408_04307_b200.arena import StateArena
     from paper_2408_04307_b200.counting import DeviceTokenCounters
     from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.staging import StagingLayout
     from paper_2408_04307_b200.store import DiskStore
 
     w, layout, plan = build_workload(args, rank)
@@ -351,11 +363,31 @@ def run_b200(args):
     sel = torch.empty((L, min(k_s, E)), dtype=torch.int32, device=dev)
     stream = eng.pack_stream
 
+    ids_step = torch.randint(0, E, (L, routed), dtype=torch.int32, device=dev,
+                             generator=torch.Generator(device=dev).manual_seed(1234 + rank))
+    pt = getattr(eng, "template", None)
+    la_bytes = None
+    if plan is None:
+        from paper_2408_04307_b200.selector import select_window as _sw
+        # payload of the load-aware steps: measured from the host mirror of
+        # each step's selection after the timed region
+        la_bytes = []
+
     def step(c):
-        """select (device) + pack of checkpoint c; returns (t0, t1, bytes)."""
-        p = plan.phase_of(c)
-        D.select_sequential(c, L, E, k_s, w.pec.k_persist, sel, stream=stream)
-        return eng.pack_only(plan.assignments[p], plan_key=("phase", p), stream=stream)
+        """One checkpoint's device work; returns (t0, t1, bytes or None).
+        sequential: select kernel + pack of the plan phase; load-aware: one
+        iteration's token histogram + two-tier selection + device plan
+        expansion + pack (no host synchronisation)."""
+        if plan is not None:
+            p = plan.phase_of(c)
+            D.select_sequential(c, L, E, k_s, w.pec.k_persist, sel, stream=stream)
+            return eng.pack_only(plan.assignments[p], plan_key=("phase", p), stream=stream)
+        with torch.cuda.stream(stream):
+            counters.add_iteration(ids_step, stream=stream)
+            snap_d, pers_d = counters.select(k_s, w.pec.k_persist, stream=stream)
+        a, b = eng.pack_only_device(snap_d, stream=stream)
+        la_bytes.append(snap_d)
+        return a, b, None
 
     for c in range(args.warmup):
         step(c)
@@ -372,13 +404,22 @@ def run_b200(args):
         for k in range(args.steps):
             a, b, n = step(args.warmup + k)
             evs.append((a, b))
-            moved += n
+            moved += n or 0
         t1.record(stream)
         stream.synchronize()
     torch.cuda.synchronize()
     barrier(world)
     elapsed_ms = t0.elapsed_time(t1)
     pack_ms = [a.elapsed_time(b) for a, b in evs]
+    if plan is None:
+        # bytes of each load-aware step from the host mirror of its selection
+        from paper_2408_04307_b200.staging import StagingLayout as _SL
+        sels = la_bytes[-args.steps:]
+        moved = 0
+        for sd in sels:
+            h = sd.cpu().tolist()
+            due = {m: frozenset(x for x in h[m] if x >= 0) for m in range(L)}
+            moved += sum(a.stop - a.start for a in pt.select(due))
     max_ms = max_over_ranks(elapsed_ms, world, dev)
     total_moved = sum_over_ranks(moved, world, dev)
     value = total_moved / (max_ms / 1e3) / 1e9
@@ -414,9 +455,12 @@ def run_b200(args):
         ids_host = [torch.from_numpy(rng.integers(0, E, size=(L, routed), dtype=np.int32)).pin_memory()
                     for _ in range(e2e_steps + 1)]
         ids_dev = torch.empty((L, routed), dtype=torch.int32, device=dev)
-        warm = torch.empty(min(eng.staging.numel(), 1 << 30), dtype=torch.uint8, pin_memory=True)
-        warm.copy_(eng.staging[:warm.numel()])
-        del warm
+        # first D2H into a freshly pinned buffer runs slow (IOMMU/page-table
+        # warm-up): touch every host buffer once before timing
+        for hb in eng.host:
+            if hb is not None:
+                n_ = min(hb.numel(), eng.staging.numel())
+                hb[:n_].copy_(eng.staging[:n_])
         barrier(world)
         torch.cuda.synchronize()
         h2d = d2h = 0
@@ -463,7 +507,11 @@ def run_b200(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
-        first_layout = eng._table_for(plan.assignments[0], ("phase", 0))[1][rank]
+        if plan is not None:
+            first_layout = eng._table_for(plan.assignments[0], ("phase", 0))[1][rank]
+        else:
+            first_layout = eng._inflight[max(eng._inflight)].layouts[rank] if eng._inflight \
+                else StagingLayout.build(pt.ranges, arena, rank)
         gbs, desc = cpu_pack_sample(first_layout.entries, int(args.cpu_sample_gb * 1e9), threads,
                                     args.cpu_seconds)
         cpu = {"value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",
@@ -475,12 +523,14 @@ def run_b200(args):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": w.name, "plan": plan.strategy, "k_pec": w.pec.k_pec,
+            "config": {"workload": w.name, "plan": w.strategy, "selection": w.pec.selection,
+                       "k_pec": w.pec.k_pec,
                        "ranks": f"0..{world - 1} of dp={layout.n_ranks}",
                        "bytes_per_step_rank0": moved // args.steps,
                        "state_resident_gb": round(arena.resident_bytes() / 1e9, 2),
                        "engine": args.engine, "chunk_log2": args.chunk_log2,
-                       "l2": "no flush needed: each step reads >= 9.9 GB (> 126 MB L2)",
+                       "l2": (f"no flush needed: each step reads "
+                              f"{(moved // args.steps) / 1e9:.2f} GB (> 126 MB L2)"),
                        "parallelism": f"dp{layout.n_ranks}-ep{layout.parallel.ep_degree}"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
@@ -499,7 +549,7 @@ def run_b200(args):
             "stall": stall,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": (2 if plan is not None else 5) * args.steps,
             "fill_s": round(t_fill, 2),
         }
         if line["host_link"]:

@@ -94,7 +94,7 @@ int pec_select_load_aware(int64_t* counters, int L, int E, int K,
  *   build_phase_assignment (planner.py:263-295).
  * descs: DEVICE table of n copies (src = state, dst = staging), chunk
  * prefix filled by pec_plan_chunks with the same chunk_log2 (12..24).
- * mode: 0 = auto, 1 = vectorised LDG/STG.128 engine, 2 = TMA bulk
+ * mode: 0 = auto (TMA bulk), 1 = vectorised LDG/STG.128 engine, 2 = TMA bulk
  * (cp.async.bulk) engine.  Ranges may be byte-granular; the fast path needs
  * src == dst (mod 16), which the staging layout guarantees. */
 int pec_pack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
@@ -106,6 +106,34 @@ int pec_pack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
  * Same table format with src = staging, dst = state. */
 int pec_unpack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
                int chunk_log2, int mode, void* stream);
+
+/* ---- device-side plan expansion (load-aware, no host round trip) ------ *
+ * Replaces: the per-checkpoint build_phase_assignment (planner.py:263-295,
+ * called from simulator.py:402-406 for load-aware selection) for one rank,
+ * for strategies whose non-expert placement does not depend on the due set
+ * (equal_pec, baseline).  tmpl is the rank's entry list with every expert
+ * due (planner order); entries with layer < 0 are always saved.  sel is the
+ * device selection [L][K] (pec_select_load_aware output).  Writes out[n]
+ * (dropped entries get nbytes 0) and totals[0] = chunks, totals[1] = staged
+ * bytes; staging offsets follow the StagingLayout rule (>= previous end,
+ * == src_offset mod stage_align).  All device memory; async. */
+typedef struct pec_plan_template {
+  uint64_t src_offset;  /* byte offset of the range in the state arena */
+  uint64_t nbytes;
+  int32_t layer;        /* MoE layer, or -1 for always-saved entries */
+  int32_t expert;
+  uint64_t reserved;
+} pec_plan_template;
+
+int pec_expand_plan(const pec_plan_template* tmpl, int n, const int32_t* sel, int L, int K,
+                    uint64_t state_base, uint64_t stage_base, int chunk_log2, int stage_align,
+                    pec_copy_desc* out, uint64_t* totals, void* stream);
+
+/* pec_pack over a device-built table whose chunk count lives in device
+ * memory (*total_chunks_dev, e.g. totals[0] of pec_expand_plan); max_chunks
+ * bounds the launch. */
+int pec_pack_indirect(const pec_copy_desc* descs, int n, uint64_t max_chunks,
+                      const uint64_t* total_chunks_dev, int chunk_log2, int mode, void* stream);
 
 /* Host helper: fill first_chunk of a HOST table in place and return the
  * total chunk count (negative PEC_E_* on bad input). */

@@ -284,11 +284,17 @@ constexpr int kVecThreads = 256;
 constexpr int kVecUnroll = 8;
 
 __global__ void __launch_bounds__(kVecThreads)
-copy_vec_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total, int lg) {
+copy_vec_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
+                const uint64_t* __restrict__ total_dev, int lg) {
+  if (total_dev != nullptr) {
+    const uint64_t t = *total_dev;  // written by pec_expand_plan earlier on the stream
+    total = t < total ? t : total;
+  }
   for (uint64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
     const int i = find_desc(d, n, ch);
     const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << lg;
     const uint64_t nb = __ldg(&d[i].nbytes);
+    if (off >= nb) continue;  // empty descriptor (never for a well-formed table)
     const uint64_t span = 1ull << lg;
     const uint64_t len = nb - off < span ? nb - off : span;
     const uint8_t* s = reinterpret_cast<const uint8_t*>(__ldg(&d[i].src) + off);
@@ -361,7 +367,7 @@ __device__ __forceinline__ ChunkView chunk_view(const pec_copy_desc* __restrict_
   const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << lg;
   const uint64_t nb = __ldg(&d[i].nbytes);
   const uint64_t span = 1ull << lg;
-  v.len = nb - off < span ? nb - off : span;
+  v.len = off >= nb ? 0 : (nb - off < span ? nb - off : span);
   v.s = reinterpret_cast<const uint8_t*>(__ldg(&d[i].src) + off);
   v.t = reinterpret_cast<uint8_t*>(__ldg(&d[i].dst) + off);
   const uintptr_t sa = reinterpret_cast<uintptr_t>(v.s);
@@ -405,8 +411,13 @@ __device__ __forceinline__ Piece piece_of(const pec_copy_desc* __restrict__ d, i
 }
 
 __global__ void __launch_bounds__(kBulkThreads, 1)
-copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total, int lg) {
+copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
+                 const uint64_t* __restrict__ total_dev, int lg) {
   extern __shared__ __align__(128) uint8_t ring[];  // kBulkStages * stage
+  if (total_dev != nullptr) {
+    const uint64_t t = *total_dev;
+    total = t < total ? t : total;
+  }
   __shared__ __align__(8) uint64_t bars[kBulkStages];
   const int piece_log2 = lg < kStageLog2 ? lg : kStageLog2;
   const uint32_t stage_bytes = 1u << piece_log2;
@@ -481,6 +492,65 @@ copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total, int
   }
 }
 
+// ------------------------------------------------------------------------
+// device-side plan expansion (load-aware snapshots without a host round trip)
+// ------------------------------------------------------------------------
+// The template is the rank's entry list for "every expert due", in the
+// reference's order (planner.py:263-295: owned, experts by (layer, expert),
+// non-expert modules).  For any due set the rank's entries are the
+// subsequence whose (layer, expert) is selected (layer < 0: always kept), so
+// one warp filters the template against sel[L][K] and lays the kept entries
+// out in staging with the StagingLayout rule (offset >= previous end and
+// == source mod align), writing a ready pec_copy_desc table (dropped
+// entries: nbytes = 0) plus {total chunks, staged bytes}.
+__global__ void expand_plan_kernel(const pec_plan_template* __restrict__ tmpl, int n,
+                                   const int32_t* __restrict__ sel, int L, int K,
+                                   uint64_t state_base, uint64_t stage_base, int lg,
+                                   uint64_t align, pec_copy_desc* __restrict__ out,
+                                   uint64_t* __restrict__ totals) {
+  const int lane = threadIdx.x;
+  uint64_t pos = 0, chunks = 0;  // meaningful in lane 0
+  const uint64_t span = 1ull << lg;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    bool keep = false;
+    if (i < n) {
+      const int layer = tmpl[i].layer;
+      if (layer < 0) {
+        keep = true;
+      } else if (layer < L) {
+        const int e = tmpl[i].expert;
+        for (int k = 0; k < K; ++k) keep |= (sel[(int64_t)layer * K + k] == e);
+      }
+    }
+    const unsigned kept = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) {
+      const int m = n - base < 32 ? n - base : 32;
+      for (int j = 0; j < m; ++j) {
+        const pec_plan_template t = tmpl[base + j];
+        pec_copy_desc dsc;
+        dsc.src = state_base + t.src_offset;
+        dsc.first_chunk = chunks;
+        if ((kept >> j) & 1u) {
+          const uint64_t off = pos + ((t.src_offset - pos) % align + align) % align;
+          dsc.dst = stage_base + off;
+          dsc.nbytes = t.nbytes;
+          pos = off + t.nbytes;
+          chunks += (t.nbytes + span - 1) / span;
+        } else {
+          dsc.dst = stage_base + pos;
+          dsc.nbytes = 0;
+        }
+        out[base + j] = dsc;
+      }
+    }
+  }
+  if (lane == 0) {
+    totals[0] = chunks;
+    totals[1] = pos;
+  }
+}
+
 // Per-device launch geometry, computed once (attribute setting and
 // occupancy queries are host round trips that would otherwise sit between
 // the caller's start event and the kernel).
@@ -514,7 +584,8 @@ int copy_geometry(CopyGeometry** out) {
   return PEC_OK;
 }
 
-int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, int lg, int mode, void* stream) {
+int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, const uint64_t* total_dev,
+                int lg, int mode, void* stream) {
   if (n < 0 || lg < 12 || lg > 24) return PEC_E_INVAL;
   if (mode < 0 || mode > 2) return PEC_E_INVAL;
   if (total == 0 || n == 0) return PEC_OK;
@@ -526,11 +597,11 @@ int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, int lg, int m
   if (mode == 2) {
     const int smem = kBulkStages << (lg < kStageLog2 ? lg : kStageLog2);
     const uint64_t grid = (uint64_t)g->bulk_grid < total ? (uint64_t)g->bulk_grid : total;
-    copy_bulk_kernel<<<(unsigned)grid, kBulkThreads, smem, st>>>(descs, n, total, lg);
+    copy_bulk_kernel<<<(unsigned)grid, kBulkThreads, smem, st>>>(descs, n, total, total_dev, lg);
     return launch_status();
   }
   const uint64_t grid = (uint64_t)g->vec_grid < total ? (uint64_t)g->vec_grid : total;
-  copy_vec_kernel<<<(unsigned)grid, kVecThreads, 0, st>>>(descs, n, total, lg);
+  copy_vec_kernel<<<(unsigned)grid, kVecThreads, 0, st>>>(descs, n, total, total_dev, lg);
   return launch_status();
 }
 
@@ -600,12 +671,30 @@ int pec_select_load_aware(int64_t* counters, int L, int E, int K,
 
 int pec_pack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
              int chunk_log2, int mode, void* stream) {
-  return launch_copy(descs, n, total_chunks, chunk_log2, mode == 0 ? 2 : mode, stream);
+  return launch_copy(descs, n, total_chunks, nullptr, chunk_log2, mode == 0 ? 2 : mode, stream);
 }
 
 int pec_unpack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
                int chunk_log2, int mode, void* stream) {
-  return launch_copy(descs, n, total_chunks, chunk_log2, mode == 0 ? 2 : mode, stream);
+  return launch_copy(descs, n, total_chunks, nullptr, chunk_log2, mode == 0 ? 2 : mode, stream);
+}
+
+int pec_pack_indirect(const pec_copy_desc* descs, int n, uint64_t max_chunks,
+                      const uint64_t* total_chunks_dev, int chunk_log2, int mode, void* stream) {
+  if (total_chunks_dev == nullptr) return PEC_E_INVAL;
+  return launch_copy(descs, n, max_chunks, total_chunks_dev, chunk_log2, mode == 0 ? 2 : mode,
+                     stream);
+}
+
+int pec_expand_plan(const pec_plan_template* tmpl, int n, const int32_t* sel, int L, int K,
+                    uint64_t state_base, uint64_t stage_base, int chunk_log2, int stage_align,
+                    pec_copy_desc* out, uint64_t* totals, void* stream) {
+  if (n < 0 || L < 1 || K < 1 || chunk_log2 < 12 || chunk_log2 > 24 || stage_align < 1) return PEC_E_INVAL;
+  if (n > 0 && (tmpl == nullptr || out == nullptr)) return PEC_E_INVAL;
+  if (sel == nullptr || totals == nullptr) return PEC_E_INVAL;
+  expand_plan_kernel<<<1, 32, 0, as_stream(stream)>>>(tmpl, n, sel, L, K, state_base, stage_base,
+                                                      chunk_log2, (uint64_t)stage_align, out, totals);
+  return launch_status();
 }
 
 int64_t pec_plan_chunks(pec_copy_desc* host_descs, int n, int chunk_log2) {

@@ -27,6 +27,9 @@ PEC_E_RANGE = -3
 # numpy mirror of `pec_copy_desc`
 DESC_DTYPE = np.dtype([("src", "<u8"), ("dst", "<u8"), ("nbytes", "<u8"),
                        ("first_chunk", "<u8")])
+# numpy mirror of `pec_plan_template`
+TEMPLATE_DTYPE = np.dtype([("src_offset", "<u8"), ("nbytes", "<u8"), ("layer", "<i4"),
+                           ("expert", "<i4"), ("reserved", "<u8")])
 DEFAULT_CHUNK_LOG2 = 15  # 32 KiB work chunks
 
 MODE_AUTO, MODE_VEC, MODE_BULK = 0, 1, 2
@@ -58,6 +61,9 @@ def _load():
         "pec_pack": (c_int, [vp, c_int, c_u64, c_int, c_int, vp]),
         "pec_unpack": (c_int, [vp, c_int, c_u64, c_int, c_int, vp]),
         "pec_plan_chunks": (c_i64, [vp, c_int, c_int]),
+        "pec_expand_plan": (c_int, [vp, c_int, vp, c_int, c_int, c_u64, c_u64, c_int, c_int,
+                                    vp, vp, vp]),
+        "pec_pack_indirect": (c_int, [vp, c_int, c_u64, vp, c_int, c_int, vp]),
         "pec_crc32c": (c_u32, [vp, ctypes.c_size_t, c_u32]),
         "pec_crc32c_combine": (c_u32, [c_u32, c_u32, c_u64]),
         "pec_crc32c_many": (c_int, [vp, vp, vp, c_int, vp, c_int]),
@@ -81,6 +87,7 @@ def exported_symbols():
     """Names declared in include/pec.h (for the ABI tests)."""
     return ["pec_abi_version", "pec_strerror", "pec_token_hist", "pec_select_sequential",
             "pec_select_load_aware", "pec_pack", "pec_unpack", "pec_plan_chunks",
+            "pec_expand_plan", "pec_pack_indirect",
             "pec_crc32c", "pec_crc32c_combine", "pec_crc32c_many"]
 
 
@@ -205,6 +212,35 @@ def pack(desc_dev, n, total_chunks, chunk_log2=DEFAULT_CHUNK_LOG2, mode=MODE_AUT
 
 def unpack(desc_dev, n, total_chunks, chunk_log2=DEFAULT_CHUNK_LOG2, mode=MODE_AUTO, stream=None):
     _copy("pec_unpack", desc_dev, n, total_chunks, chunk_log2, mode, stream)
+
+
+def expand_plan(tmpl_dev, n: int, sel, state_base: int, stage_base: int, out_dev, totals_dev,
+                chunk_log2: int = DEFAULT_CHUNK_LOG2, stage_align: int = 256, stream=None) -> None:
+    """Device-side plan expansion (pec_expand_plan): filter the rank's
+    all-experts template by sel [L, K] into a ready descriptor table."""
+    import torch
+    if stage_align & (stage_align - 1):
+        raise SpecValidationError("stage_align is a power of two", str(stage_align))
+    L, K = sel.shape
+    rc = lib().pec_expand_plan(_dev_ptr(tmpl_dev, tmpl_dev.dtype, "template"), n,
+                               _dev_ptr(sel, torch.int32, "sel", 2), L, K, state_base, stage_base,
+                               chunk_log2, stage_align,
+                               _dev_ptr(out_dev, out_dev.dtype, "descriptor table"),
+                               _dev_ptr(totals_dev, torch.int64, "totals"),
+                               _stream_handle(stream, sel.device))
+    _check(rc, "pec_expand_plan")
+
+
+def pack_indirect(desc_dev, n: int, max_chunks: int, totals_dev,
+                  chunk_log2: int = DEFAULT_CHUNK_LOG2, mode: int = MODE_AUTO, stream=None) -> None:
+    """pec_pack over a device-built table; chunk count read from totals_dev[0]."""
+    import torch
+    if n == 0 or max_chunks == 0:
+        return
+    rc = lib().pec_pack_indirect(_dev_ptr(desc_dev, desc_dev.dtype, "descriptor table"), n,
+                                 max_chunks, _dev_ptr(totals_dev, torch.int64, "totals"),
+                                 chunk_log2, mode, _stream_handle(stream, desc_dev.device))
+    _check(rc, "pec_pack_indirect")
 
 
 # ---------------------------------------------------------------------------

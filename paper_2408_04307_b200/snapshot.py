@@ -55,7 +55,7 @@ from .planner import (
     plan_equal,
 )
 from .selector import select_window
-from .staging import DeviceTable, StagingLayout
+from .staging import DeviceTable, PlanTemplate, StagingLayout
 from .store import StoreEntry
 from .topology import RankLayout
 
@@ -194,6 +194,99 @@ class DeviceCheckpointEngine(CheckpointEngine):
         self.stats["snap_bytes"].append(sum(l.payload_bytes for l in layouts.values()))
         return buf
 
+    # -- device-planned snapshots (load-aware: no host round trip before the pack)
+    def enable_device_plans(self, strategy: str) -> None:
+        """Build this rank's all-experts template once; afterwards
+        `begin_snapshot_device` expands the plan on the GPU from a device
+        selection (equal_pec / baseline; one local rank)."""
+        import torch
+        if len(self.ranks) != 1:
+            raise ValueError("device plans need exactly one local rank per engine")
+        self.strategy = strategy
+        self.template = PlanTemplate(self.layout, self.arena, self.ranks[0], strategy, self.device)
+        self._ensure_staging(self.template.max_bytes)
+        self._dev_table = torch.empty(max(1, self.template.n) * 4, dtype=torch.int64,
+                                      device=self.device)
+        self._dev_totals = torch.zeros(2, dtype=torch.int64, device=self.device)
+        self._meta_stream = torch.cuda.Stream(device=self.device)
+
+    def _expand_and_pack(self, snap_sel_dev, stream):
+        import torch
+        t = self.template
+        D.expand_plan(t.tensor, t.n, snap_sel_dev, self.arena.base_address,
+                      self.staging.data_ptr(), self._dev_table, self._dev_totals,
+                      self.chunk_log2, stream=stream)
+        expanded = torch.cuda.Event()
+        expanded.record(stream)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        D.pack_indirect(self._dev_table, t.n, t.max_chunks(self.chunk_log2), self._dev_totals,
+                        self.chunk_log2, self.pack_mode, stream=stream)
+        t1.record(stream)
+        return expanded, t0, t1
+
+    def pack_only_device(self, snap_sel_dev, stream=None):
+        """Device-only step of a load-aware snapshot: expand + pack, no drain,
+        no host synchronisation.  Returns (start_event, end_event)."""
+        s = stream or self.pack_stream
+        if self._staging_free is not None:
+            s.wait_event(self._staging_free)
+        _, t0, t1 = self._expand_and_pack(snap_sel_dev, s)
+        return t0, t1
+
+    def begin_snapshot_device(self, iteration: int, checkpoint_index: int, snap_sel_dev,
+                              persist_sel_dev, compute_stream=None):
+        """Load-aware snapshot from device selections [L, k_s] / [L, k_p]:
+        expand + pack are enqueued at once; the host then waits only for the
+        tiny selection/size copy (not for the pack) to size the drain and to
+        fill the buffer's reference-format content.  Returns (buffer,
+        persist due map)."""
+        import torch
+        from .planner import build_phase_assignment
+        rank = self.ranks[0]
+        buf = CheckpointEngine.begin_snapshot(self, iteration, checkpoint_index, None)
+        compute = compute_stream or torch.cuda.current_stream(self.device)
+        ps, cs, ms = self.pack_stream, self.copy_stream, self._meta_stream
+        ps.wait_stream(compute)
+        if self._staging_free is not None:
+            ps.wait_event(self._staging_free)
+        expanded, t0, t1 = self._expand_and_pack(snap_sel_dev, ps)
+        # small D2H of {chunks, bytes} and both selections on a side stream
+        ms.wait_event(expanded)
+        L = snap_sel_dev.shape[0]
+        meta = torch.empty(2 + snap_sel_dev.numel() + persist_sel_dev.numel(), dtype=torch.int64,
+                           pin_memory=True)
+        with torch.cuda.stream(ms):
+            meta[:2].copy_(self._dev_totals, non_blocking=True)
+            meta[2:2 + snap_sel_dev.numel()].copy_(snap_sel_dev.reshape(-1), non_blocking=True)
+            meta[2 + snap_sel_dev.numel():].copy_(persist_sel_dev.reshape(-1), non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record(ms)
+        ready.synchronize()
+        nbytes = int(meta[1])
+        snap_h = meta[2:2 + snap_sel_dev.numel()].view(L, -1).tolist()
+        pers_h = meta[2 + snap_sel_dev.numel():].view(L, -1).tolist()
+        due = {m: frozenset(e for e in snap_h[m] if e >= 0) for m in range(L)}
+        persist_due = {m: frozenset(e for e in pers_h[m] if e >= 0) for m in range(L)}
+        assignment = build_phase_assignment(self.layout, due, self.strategy)
+        buf.content = assignment
+        layout = StagingLayout.build(assignment.get(rank, ()), self.arena, rank)
+        if layout.nbytes != nbytes:
+            raise RuntimeError(f"device plan ({nbytes} B) disagrees with host plan "
+                               f"({layout.nbytes} B)")
+        host = self._ensure_host(buf.buffer_id, nbytes)
+        rec = _Inflight({rank: layout}, {rank: 0}, nbytes, t_begin=time.perf_counter())
+        rec.pack_start, rec.pack_done = t0, t1
+        cs.wait_event(t1)
+        rec.drain_done = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(cs):
+            host[:nbytes].copy_(self.staging[:nbytes], non_blocking=True)
+        rec.drain_done.record(cs)
+        self._staging_free = rec.drain_done
+        self._inflight[buf.buffer_id] = rec
+        self.stats["snap_bytes"].append(layout.payload_bytes)
+        return buf, persist_due
+
     def wait_pack(self, buf: Optional[Buffer] = None, stream=None) -> None:
         """Make ``stream`` (default: current) wait for the pack of ``buf`` (or
         the latest snapshot) before it modifies the state."""
@@ -226,8 +319,8 @@ class DeviceCheckpointEngine(CheckpointEngine):
         return memoryview(host[off:off + e.nbytes])
 
     def payloads(self, buf: Buffer, entries: Iterable[StoreEntry]) -> Dict[str, memoryview]:
-        return {e.store_key: self.entry_view(buf, e.rank, e.store_key) for e in entries
-                if e.rank in self.ranks}
+        return {e.store_key: (self.entry_view(buf, e.rank, e.store_key) if e.stop > e.start
+                              else memoryview(b"")) for e in entries if e.rank in self.ranks}
 
     def has_bytes(self, buf: Buffer) -> bool:
         return buf.buffer_id in self._inflight
@@ -307,6 +400,7 @@ class PecCheckpointer:
         self.persist_sel: Dict[int, Dict[int, frozenset]] = {}
         self._plan: Optional[ShardPlan] = None
         self.stall_s = 0.0
+        self.device_plans = False
         if pec is not None and pec.selection == LOAD_AWARE:
             if strategy == ADAPTIVE_PEC:
                 from .topology import SpecValidationError
@@ -314,6 +408,9 @@ class PecCheckpointer:
                                           "load-aware selection is not periodic")
             if counters is None:
                 raise ValueError("load-aware selection needs DeviceTokenCounters")
+            if len(self.engine.ranks) == 1:
+                self.engine.enable_device_plans(strategy)
+                self.device_plans = True
 
     # -- plans --------------------------------------------------------------------
     def plan(self) -> Optional[ShardPlan]:
@@ -369,6 +466,8 @@ class PecCheckpointer:
 
     def checkpoint(self, iteration: int) -> Buffer:
         c = iteration // self.i_ckpt - 1
+        if self.device_plans:
+            return self._checkpoint_device(iteration, c)
         snap_sel, persist_sel = self.selections(c)
         plan = self.plan()
         if plan is not None:
@@ -392,6 +491,26 @@ class PecCheckpointer:
                     raise
                 self.stall_s += time.perf_counter() - t0
         self.persist_sel[buf.version] = persist_sel
+        return buf
+
+    def _checkpoint_device(self, iteration: int, c: int) -> Buffer:
+        """Load-aware checkpoint with selection and plan on the GPU."""
+        while True:
+            snapping = self.engine.buffers.snapshotting
+            if snapping is not None:
+                t0 = time.perf_counter()
+                self._complete(snapping)
+                self.stall_s += time.perf_counter() - t0
+            if any(b.status == "free" for b in self.engine.buffers.buffers):
+                break
+            t0 = time.perf_counter()
+            if not self._wait_one_persist():
+                raise NoFreeBufferError("no free buffer and no persist in flight")
+            self.stall_s += time.perf_counter() - t0
+        snap_d, pers_d = self.counters.select(self.pec.k_snapshot, self.pec.k_persist,
+                                              group=self.group)
+        buf, persist_due = self.engine.begin_snapshot_device(iteration, c, snap_d, pers_d)
+        self.persist_sel[buf.version] = persist_due
         return buf
 
     def wait_pack(self, stream=None) -> None:

@@ -23,7 +23,7 @@ from typing import Iterable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .device import DEFAULT_CHUNK_LOG2, DESC_DTYPE, plan_chunks
+from .device import DEFAULT_CHUNK_LOG2, DESC_DTYPE, TEMPLATE_DTYPE, plan_chunks
 from .planner import RangeAssignment
 
 STAGE_ALIGN = 256
@@ -106,3 +106,48 @@ class DeviceTable:
             torch.zeros(DESC_DTYPE.itemsize, dtype=torch.uint8)
         self.tensor = raw.view(torch.int64).to(device)
         self.nbytes_moved = int(table["nbytes"].sum()) if self.n else 0
+
+
+class PlanTemplate:
+    """A rank's entry list with every expert due, in planner order, for the
+    device-side plan expansion (`pec_expand_plan`).
+
+    For strategies whose non-expert placement does not depend on the due set
+    (equal_*, baseline), the rank's entries for ANY due set are exactly the
+    template entries whose (layer, expert) is due, in template order
+    (`_expert_entries` iterates due layers/experts in sorted order,
+    planner.py:213-240), plus every owned / non-expert entry."""
+
+    def __init__(self, layout, arena, rank: int, strategy: str, device):
+        import torch
+        from .planner import ADAPTIVE_PEC, build_phase_assignment, full_due_map
+        if strategy == ADAPTIVE_PEC:
+            raise ValueError("adaptive placement depends on the due set; no device template")
+        self.rank = rank
+        self.strategy = strategy
+        self.layout = layout
+        self.ranges = tuple(a for a in build_phase_assignment(layout, full_due_map(layout),
+                                                              strategy).get(rank, ())
+                            if a.stop > a.start)  # empty ranges carry no bytes
+        table = np.zeros(len(self.ranges), dtype=TEMPLATE_DTYPE)
+        for i, a in enumerate(self.ranges):
+            u = layout.by_key[a.key]
+            table[i]["src_offset"] = arena.slot(a.key).offset + a.start
+            table[i]["nbytes"] = a.stop - a.start
+            table[i]["layer"] = -1 if u.layer is None else u.layer
+            table[i]["expert"] = -1 if u.expert is None else u.expert
+        self.table = table
+        self.n = len(table)
+        self.max_bytes = StagingLayout.build(self.ranges, arena, rank).nbytes
+        self.tensor = torch.from_numpy(table.view(np.uint8).copy()).view(torch.int64).to(device) \
+            if self.n else torch.zeros(4, dtype=torch.int64, device=device)
+
+    def max_chunks(self, chunk_log2: int = DEFAULT_CHUNK_LOG2) -> int:
+        span = 1 << chunk_log2
+        return int(sum((int(n) + span - 1) // span for n in self.table["nbytes"]))
+
+    def select(self, due) -> tuple:
+        """The rank's RangeAssignments for a due map (host mirror of the
+        device filter)."""
+        return tuple(a for a, t in zip(self.ranges, self.table)  # noqa: E501
+                     if t["layer"] < 0 or int(t["expert"]) in due.get(int(t["layer"]), ()))

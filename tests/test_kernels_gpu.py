@@ -204,3 +204,46 @@ def test_pack_plan_phases_bit_exact(dev, mode):
                 copies = [(e.src_offset, e.stage_offset, e.nbytes) for e in st.entries]
                 assert np.array_equal(got, O.pack(host_state, copies, st.nbytes + 1))
                 assert st.payload_bytes == plan.workload_bytes[plan.assignments.index(phase)][rank]
+
+
+@pytest.mark.parametrize("strategy", ["equal_pec", "baseline"])
+def test_device_plan_expansion_matches_host_plan(dev, strategy):
+    """pec_expand_plan + pec_pack_indirect == host build_phase_assignment +
+    StagingLayout + oracle pack, for random selections on a 2-EP-group layout
+    (byte-split expert weights), every rank."""
+    import torch
+    from paper_2408_04307_b200 import build_phase_assignment
+    from paper_2408_04307_b200 import device as D
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.staging import PlanTemplate, StagingLayout
+    layout = make_layout(n_experts=8, dp=4, ep=2, n_layers=3, epp=20_001, p_ne=3_001, other=9,
+                         modules=(("a", 1000), ("b", 1001), ("c", 1000)))
+    L, E = 3, 8
+    rng = np.random.default_rng(7)
+    for rank in range(4):
+        arena = StateArena(layout, [rank], dev)
+        host_state = arena.buffer.cpu().numpy()
+        tmpl = PlanTemplate(layout, arena, rank, strategy, dev)
+        staging = torch.zeros(tmpl.max_bytes + 512, dtype=torch.uint8, device=dev)
+        table = torch.empty(max(1, tmpl.n) * 4, dtype=torch.int64, device=dev)
+        totals = torch.zeros(2, dtype=torch.int64, device=dev)
+        for trial in range(6):
+            k = int(rng.integers(1, E + 1))
+            sel = np.stack([np.sort(rng.choice(E, size=k, replace=False)) for _ in range(L)])
+            sel_d = torch.from_numpy(sel.astype(np.int32)).to(dev)
+            staging.zero_()
+            D.expand_plan(tmpl.tensor, tmpl.n, sel_d, arena.base_address, staging.data_ptr(),
+                          table, totals)
+            D.pack_indirect(table, tmpl.n, tmpl.max_chunks(), totals)
+            torch.cuda.synchronize()
+            due = {m: frozenset(int(x) for x in sel[m]) for m in range(L)}
+            ranges = build_phase_assignment(layout, due, strategy).get(rank, ())
+            st = StagingLayout.build(ranges, arena, rank)
+            assert tuple(a for a in ranges if a.stop > a.start) == tmpl.select(due)
+            assert int(totals[1]) == st.nbytes
+            _, nch = st.descriptors(0, 0)
+            assert int(totals[0]) == nch
+            copies = [(e.src_offset, e.stage_offset, e.nbytes) for e in st.entries]
+            want = O.pack(host_state, copies, tmpl.max_bytes + 512)
+            assert np.array_equal(staging.cpu().numpy(), want), (rank, trial)
+        del arena
