@@ -5,20 +5,26 @@ The reference decides, per unit, where its newest full copy lives
 bytes.  Here the decisions are executed:
 
   memory   the unit's ranges are copied H2D straight out of the pinned host
-           snapshot buffer of the decided version (the two-level engine's
-           in-memory copy; engine.py:214-229),
-  storage  the unit's entry files of the decided version are read (CRC
-           verified, DiskStore.load_checkpoint semantics, store.py:267-282)
-           into a pinned restore buffer, then copied H2D,
+           snapshot buffer of the decided version on the decided (surviving)
+           node (the two-level engine's in-memory copy; engine.py:214-229),
+  storage  the unit's entry files of the decided version are read into a
+           pinned bounce slot, CRC-32C verified against the manifest
+           (DiskStore.load_checkpoint semantics, store.py:267-282), and
+           copied H2D,
   initial  experts never saved anywhere are regenerated from their seed
            (arena.fill_unit).
 
-All restored ranges then go through ONE `pec_unpack` launch that scatters
-them from the device restore staging into the state arena.
+Streaming: pieces are grouped into batches of at most ``slot_bytes``; two
+pinned host slots and two device slots alternate, so file reads of batch
+i+1 (a host thread pool) overlap the H2D copy and the `pec_unpack` scatter
+of batch i into the state arena (one launch per batch).  Entries larger
+than a slot are split; their CRC is chained across the pieces.
 """
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from typing import Dict, Iterable, List, Optional, Tuple
 
@@ -27,6 +33,7 @@ import numpy as np
 from . import device as D
 from .engine import RecoveryPlan
 from .staging import STAGE_ALIGN, DeviceTable
+from .store import ChecksumMismatchError, crc32c
 
 
 @dataclass
@@ -35,114 +42,224 @@ class RestoreReport:
     memory_bytes: int
     storage_bytes: int
     initial_units: int
-    unpack_ms: float
+    unpack_ms: float      # sum of the per-batch unpack kernel times
+    batches: int = 0
+    wall_s: float = 0.0
+
+
+@dataclass
+class _Piece:
+    unit: str
+    start: int            # byte range of the unit image
+    stop: int
+    kind: str             # "file" | "host" | "bytes"
+    path: Optional[str] = None       # file pieces
+    file_off: int = 0
+    entry: Optional[str] = None
+    entry_crc: int = 0
+    last: bool = False
+    host: object = None              # host pieces: pinned tensor + offset
+    host_off: int = 0
+
+    @property
+    def nbytes(self) -> int:
+        return self.stop - self.start
 
 
 def _place(pos: int, src_offset: int, align: int = STAGE_ALIGN) -> int:
     return pos + ((src_offset - pos) % align)
 
 
-def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
-            chunk_log2: int = D.DEFAULT_CHUNK_LOG2, stream=None) -> RestoreReport:
-    """Execute ``plan`` for the units resident in ``engine.arena`` (or the
-    given subset ``keys``).  ``engine`` is a DeviceCheckpointEngine."""
-    import torch
-    arena = engine.arena
-    store = engine.store
-    dev = arena.device
-    wanted = [k for k in (keys if keys is not None else plan.decisions) if arena.has(k)]
+class _Ring:
+    """Two pinned host slots + two device slots, allocated once per engine."""
 
-    # (unit, start, stop, host source) pieces; host source = (array, offset)
-    mem_pieces: List[Tuple[str, int, int, object, int]] = []
-    by_version: Dict[int, List[Tuple[str, object]]] = {}
-    initial = []
+    def __init__(self, device, slot_bytes: int):
+        import torch
+        self.slot_bytes = slot_bytes
+        self.host = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        self.dev = [torch.empty(slot_bytes, dtype=torch.uint8, device=device) for _ in range(2)]
+        self.free = [None, None]   # event: slot's H2D + unpack finished
+
+
+def _ring(engine, slot_bytes: int) -> _Ring:
+    r = getattr(engine, "_restore_ring", None)
+    if r is None or r.slot_bytes < slot_bytes:
+        r = _Ring(engine.device, slot_bytes)
+        engine._restore_ring = r
+    return r
+
+
+def _pieces(engine, plan: RecoveryPlan, wanted, slot_bytes: int):
+    """Expand decisions into ordered pieces (entries split at slot size)."""
+    arena, store, layout = engine.arena, engine.store, engine.layout
+    step = slot_bytes - STAGE_ALIGN
+    pieces: List[_Piece] = []
+    initial: List[str] = []
+    metas: Dict[int, object] = {}
+    manifests: Dict[int, object] = {}
     for key in wanted:
         d = plan.decisions[key]
         if d.source == "initial":
             initial.append(key)
-        elif d.source == "memory":
+            continue
+        if d.source == "memory":
             buf = next((b for b in engine.buffers.buffers
                         if b.version == d.version and b.snapshot_completed), None)
             if buf is None or not engine.has_bytes(buf):
                 raise RuntimeError(f"memory source v{d.version} for {key} is not in this process")
             rec = engine._inflight[buf.buffer_id]
-            host = engine.host[buf.buffer_id]  # pinned: H2D slices stay async
             found = False
             for r, st in rec.layouts.items():
-                if engine.layout.node_of_rank(r) != d.node:
+                if layout.node_of_rank(r) != d.node:
                     continue  # only the decided (surviving) node's copy
                 for e in st.entries:
-                    if e.unit_key == key:
-                        mem_pieces.append((key, e.start, e.stop, host, rec.region[r] + e.stage_offset))
-                        found = True
+                    if e.unit_key != key:
+                        continue
+                    found = True
+                    base = rec.region[r] + e.stage_offset
+                    for lo in range(e.start, e.stop, step):
+                        hi = min(e.stop, lo + step)
+                        pieces.append(_Piece(key, lo, hi, "host", host=engine.host[buf.buffer_id],
+                                             host_off=base + (lo - e.start)))
             if not found:
                 raise RuntimeError(f"unit {key} not held in this process's buffer v{d.version}")
-        else:
-            by_version.setdefault(d.version, []).append(key)
+            continue
+        v = d.version
+        if v not in metas:
+            metas[v] = store.meta(v)
+            manifests[v] = store.manifest(v)
+        if not hasattr(store, "version_dir"):  # MemoryStore: verified bytes in RAM
+            for sk, e in sorted(metas[v].entries.items()):
+                if e.unit_key == key:
+                    data = store.load_checkpoint(v, [sk])[sk]
+                    for lo in range(e.start, e.stop, step):
+                        hi = min(e.stop, lo + step)
+                        pieces.append(_Piece(key, lo, hi, "bytes", host=data,
+                                             host_off=lo - e.start))
+            continue
+        vdir = store.version_dir(v)
+        for sk, e in sorted(metas[v].entries.items()):
+            if e.unit_key != key:
+                continue
+            rel, size, crc = manifests[v].entries[sk]
+            path = str(vdir / rel)
+            if not os.path.exists(path):
+                raise ChecksumMismatchError(sk, "entry file missing")
+            if os.path.getsize(path) != size or size != e.stop - e.start:
+                raise ChecksumMismatchError(sk, f"size {os.path.getsize(path)} != manifest {size}")
+            for lo in range(e.start, e.stop, step):
+                hi = min(e.stop, lo + step)
+                pieces.append(_Piece(key, lo, hi, "file", path=path, file_off=lo - e.start,
+                                     entry=sk, entry_crc=crc, last=hi == e.stop))
+    return pieces, initial
 
-    # storage pieces: entry files of each version, read into one pinned buffer
-    sto_pieces: List[Tuple[str, int, int, int]] = []  # unit, start, stop, restore-host offset
-    placements: Dict[int, Dict[str, Tuple[object, int]]] = {}
-    pos = 0
-    for version, units in sorted(by_version.items()):
-        meta = store.meta(version)
-        uset = set(units)
-        for sk, e in sorted(meta.entries.items()):
-            if e.unit_key in uset:
-                src = arena.slot(e.unit_key).offset + e.start
-                off = _place(pos, src)
-                placements.setdefault(version, {})[sk] = off
-                sto_pieces.append((e.unit_key, e.start, e.stop, off))
-                pos = off + (e.stop - e.start)
-    # memory pieces follow in the same device staging
-    mem_off = []
-    for key, start, stop, host, hoff in mem_pieces:
-        src = arena.slot(key).offset + start
-        off = _place(pos, src)
-        mem_off.append(off)
-        pos = off + (stop - start)
-    total = pos
 
+_READ_STEP = 4 << 20  # CRC each 4 MiB right after reading it, while cache-hot
+
+
+def _read_piece(item) -> int:
+    p, off, host = item
+    view = memoryview(host.numpy()).cast("B")[off:off + p.nbytes]
+    crc = 0
+    with open(p.path, "rb", buffering=0) as f:
+        f.seek(p.file_off)
+        got = 0
+        while got < p.nbytes:
+            want = min(_READ_STEP, p.nbytes - got)
+            n = f.readinto(view[got:got + want])
+            if not n:
+                raise ChecksumMismatchError(p.entry, "short read")
+            crc = crc32c(view[got:got + n], crc)
+            got += n
+    return crc
+
+
+def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
+            chunk_log2: int = D.DEFAULT_CHUNK_LOG2, stream=None,
+            slot_bytes: int = 256 << 20, io_threads: int = 16) -> RestoreReport:
+    """Execute ``plan`` for the units resident in ``engine.arena`` (or the
+    given subset ``keys``).  ``engine`` is a DeviceCheckpointEngine whose
+    ``store`` (a DiskStore) holds the storage versions."""
+    import time
+    import torch
+    t_start = time.perf_counter()
+    arena = engine.arena
+    dev = arena.device
+    wanted = [k for k in (keys if keys is not None else plan.decisions) if arena.has(k)]
+    slot_bytes = max(1 << 20, slot_bytes)
+    pieces, initial = _pieces(engine, plan, wanted, slot_bytes)
     for key in initial:
         arena.fill_unit(key)
-    if total == 0:
+    rep = RestoreReport(len(wanted), 0, 0, len(initial), 0.0)
+    if not pieces:
         torch.cuda.synchronize(dev)
-        return RestoreReport(len(wanted), 0, 0, len(initial), 0.0)
+        rep.wall_s = time.perf_counter() - t_start
+        return rep
 
-    stage = torch.empty(total, dtype=torch.uint8, device=dev)
-    s = stream or torch.cuda.current_stream(dev)
-    sto_bytes = 0
-    if placements:
-        rhost = torch.empty(total, dtype=torch.uint8, pin_memory=True)
-        harr = rhost.numpy()
-        for version, pl in placements.items():
-            store.read_into(version, {k: (harr, off) for k, off in pl.items()})
-        sto_end = max(off + (stop - start) for _, start, stop, off in sto_pieces)
-        with torch.cuda.stream(s):
-            stage[:sto_end].copy_(rhost[:sto_end], non_blocking=True)
-        sto_bytes = sum(stop - start for _, start, stop, _ in sto_pieces)
-    mem_bytes = 0
-    with torch.cuda.stream(s):
-        for (key, start, stop, host, hoff), off in zip(mem_pieces, mem_off):
-            n = stop - start
-            stage[off:off + n].copy_(host[hoff:hoff + n], non_blocking=True)
-            mem_bytes += n
+    # batches of pieces, each laid out like a staging buffer (congruent mod 256)
+    batches: List[List[Tuple[_Piece, int]]] = []
+    cur: List[Tuple[_Piece, int]] = []
+    pos = 0
+    for p in pieces:
+        off = _place(pos, arena.slot(p.unit).offset + p.start)
+        if cur and off + p.nbytes > slot_bytes:
+            batches.append(cur)
+            cur = []
+            off = _place(0, arena.slot(p.unit).offset + p.start)
+        cur.append((p, off))
+        pos = off + p.nbytes
+    if cur:
+        batches.append(cur)
 
-    # one unpack over every restored range
-    pieces = [(k, a, b, off) for k, a, b, off in sto_pieces] + \
-        [(k, a, b, off) for (k, a, b, _, _), off in zip(mem_pieces, mem_off)]
-    table = np.zeros(len(pieces), dtype=D.DESC_DTYPE)
-    for i, (k, a, b, off) in enumerate(pieces):
-        table[i]["src"] = stage.data_ptr() + off
-        table[i]["dst"] = arena.base_address + arena.slot(k).offset + a
-        table[i]["nbytes"] = b - a
-    nchunks = D.plan_chunks(table, chunk_log2)
-    dt = DeviceTable(table, nchunks, dev, chunk_log2)
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record(s)
-    D.unpack(dt.tensor, dt.n, dt.total_chunks, chunk_log2, engine.pack_mode, stream=s)
-    t1.record(s)
-    t1.synchronize()
-    if placements:
-        del rhost
-    return RestoreReport(len(wanted), mem_bytes, sto_bytes, len(initial), t0.elapsed_time(t1))
+    ring = _ring(engine, slot_bytes)
+    s = stream or torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream(dev))  # e.g. initial fills / prior wipes
+    running: Dict[str, int] = {}   # entry -> chained CRC of the pieces read so far
+    timers = []
+    with ThreadPoolExecutor(max_workers=io_threads) as pool:
+        for bi, batch in enumerate(batches):
+            slot = bi % 2
+            if ring.free[slot] is not None:
+                ring.free[slot].synchronize()   # slot's previous batch fully consumed
+            hslot, dslot = ring.host[slot], ring.dev[slot]
+            files = [(p, off, hslot) for p, off in batch if p.kind == "file"]
+            crcs = list(pool.map(_read_piece, files))
+            for p, off in batch:
+                if p.kind == "bytes":
+                    hslot.numpy()[off:off + p.nbytes] = np.frombuffer(
+                        p.host, dtype=np.uint8)[p.host_off:p.host_off + p.nbytes]
+                    rep.storage_bytes += p.nbytes
+            files_or_bytes = [(p, off) for p, off in batch if p.kind in ("file", "bytes")]
+            for (p, _, _), c in zip(files, crcs):
+                prev = running.get(p.entry)
+                running[p.entry] = c if prev is None else D.crc32c_combine(prev, c, p.nbytes)
+                if p.last and running.pop(p.entry) != p.entry_crc:
+                    raise ChecksumMismatchError(p.entry, "crc32c mismatch")
+                rep.storage_bytes += p.nbytes
+            table = np.zeros(len(batch), dtype=D.DESC_DTYPE)
+            with torch.cuda.stream(s):
+                if files_or_bytes:
+                    end = max(off + p.nbytes for p, off in files_or_bytes)
+                    dslot[:end].copy_(hslot[:end], non_blocking=True)
+                for i, (p, off) in enumerate(batch):
+                    if p.kind == "host":
+                        dslot[off:off + p.nbytes].copy_(p.host[p.host_off:p.host_off + p.nbytes],
+                                                        non_blocking=True)
+                        rep.memory_bytes += p.nbytes
+                    table[i]["src"] = dslot.data_ptr() + off
+                    table[i]["dst"] = arena.base_address + arena.slot(p.unit).offset + p.start
+                    table[i]["nbytes"] = p.nbytes
+            nchunks = D.plan_chunks(table, chunk_log2)
+            dt = DeviceTable(table, nchunks, dev, chunk_log2)
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(s)
+            D.unpack(dt.tensor, dt.n, dt.total_chunks, chunk_log2, engine.pack_mode, stream=s)
+            t1.record(s)
+            timers.append((t0, t1, dt))
+            ring.free[slot] = t1
+    torch.cuda.current_stream(dev).wait_stream(s)
+    s.synchronize()
+    rep.unpack_ms = sum(a.elapsed_time(b) for a, b, _ in timers)
+    rep.batches = len(batches)
+    rep.wall_s = time.perf_counter() - t_start
+    return rep
