@@ -60,6 +60,31 @@ def _crc(key: str) -> int:
     return crc32c(key.encode())
 
 
+def arena_slots(layout: RankLayout, ranks: Sequence[int]) -> Dict[str, UnitSlot]:
+    """Deterministic arena placement of the units resident on ``ranks``
+    (unit order of the layout, 256-byte aligned, empty units skipped).  Any
+    process can recompute a peer rank's offsets from the layout alone."""
+    rs = set(int(r) for r in ranks)
+    slots: Dict[str, UnitSlot] = {}
+    off = 0
+    for u in layout.units:
+        if u.size_bytes == 0 or not (u.replica_ranks & rs):
+            continue
+        slots[u.key] = UnitSlot(u.key, u.kind, off, u.size_bytes)
+        off = _align(off + u.size_bytes)
+    return slots
+
+
+class PeerSlots:
+    """`slot()` lookup of a peer rank's arena (no allocation)."""
+
+    def __init__(self, layout: RankLayout, rank: int):
+        self.slots = arena_slots(layout, [rank])
+
+    def slot(self, key: str) -> UnitSlot:
+        return self.slots[key]
+
+
 class StateArena:
     """Device-resident images of the units a set of ranks holds.
 
@@ -79,14 +104,9 @@ class StateArena:
         self.expert_tensors: Tuple[Tuple[str, int], ...] = tuple(expert_tensors) or (("w", epp),)
         if epp and sum(c for _, c in self.expert_tensors) != epp:
             raise ValueError("expert_tensors must sum to expert_params_per_expert")
-        self.slots: Dict[str, UnitSlot] = {}
-        off = 0
-        for u in layout.units:
-            if u.size_bytes == 0 or not (u.replica_ranks & set(self.ranks)):
-                continue
-            self.slots[u.key] = UnitSlot(u.key, u.kind, off, u.size_bytes)
-            off = _align(off + u.size_bytes)
-        self.nbytes = max(off, ARENA_ALIGN)
+        self.slots: Dict[str, UnitSlot] = arena_slots(layout, self.ranks)
+        end = max((s.offset + s.size for s in self.slots.values()), default=0)
+        self.nbytes = max(_align(end), ARENA_ALIGN)
         self.buffer = torch.empty(self.nbytes, dtype=torch.uint8, device=self.device)
         if fill:
             self.fill_all()

@@ -97,6 +97,7 @@ def _pieces(engine, plan: RecoveryPlan, wanted, slot_bytes: int):
     initial: List[str] = []
     metas: Dict[int, object] = {}
     manifests: Dict[int, object] = {}
+    peers: Dict[Tuple[int, int], object] = {}
     for key in wanted:
         d = plan.decisions[key]
         if d.source == "initial":
@@ -109,17 +110,28 @@ def _pieces(engine, plan: RecoveryPlan, wanted, slot_bytes: int):
                 raise RuntimeError(f"memory source v{d.version} for {key} is not in this process")
             rec = engine._inflight[buf.buffer_id]
             found = False
-            for r, st in rec.layouts.items():
-                if layout.node_of_rank(r) != d.node:
-                    continue  # only the decided (surviving) node's copy
+            for r in layout.ranks_of_node(d.node):  # only the decided (surviving) node
+                if r in rec.layouts:                 # this process's pinned buffer: H2D
+                    st, base0, kind = rec.layouts[r], rec.region[r], "host"
+                    src = engine.host[buf.buffer_id]
+                else:                                # a peer process's node-shared buffer
+                    peer = peers.get((r, d.version))
+                    if peer is None and (r, d.version) not in peers:
+                        peer = engine.peer_buffer(r, d.version) if hasattr(engine, "peer_buffer") \
+                            else None
+                        peers[(r, d.version)] = peer
+                    if peer is None:
+                        continue
+                    src, st = peer[0].array, peer[1]
+                    base0, kind = 0, "bytes"
                 for e in st.entries:
                     if e.unit_key != key:
                         continue
                     found = True
-                    base = rec.region[r] + e.stage_offset
+                    base = base0 + e.stage_offset
                     for lo in range(e.start, e.stop, step):
                         hi = min(e.stop, lo + step)
-                        pieces.append(_Piece(key, lo, hi, "host", host=engine.host[buf.buffer_id],
+                        pieces.append(_Piece(key, lo, hi, kind, host=src,
                                              host_off=base + (lo - e.start)))
             if not found:
                 raise RuntimeError(f"unit {key} not held in this process's buffer v{d.version}")
@@ -151,7 +163,7 @@ def _pieces(engine, plan: RecoveryPlan, wanted, slot_bytes: int):
                 hi = min(e.stop, lo + step)
                 pieces.append(_Piece(key, lo, hi, "file", path=path, file_off=lo - e.start,
                                      entry=sk, entry_crc=crc, last=hi == e.stop))
-    return pieces, initial
+    return pieces, initial, peers
 
 
 _READ_STEP = 4 << 20  # CRC each 4 MiB right after reading it, while cache-hot
@@ -187,7 +199,7 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
     dev = arena.device
     wanted = [k for k in (keys if keys is not None else plan.decisions) if arena.has(k)]
     slot_bytes = max(1 << 20, slot_bytes)
-    pieces, initial = _pieces(engine, plan, wanted, slot_bytes)
+    pieces, initial, peers = _pieces(engine, plan, wanted, slot_bytes)
     for key in initial:
         arena.fill_unit(key)
     rep = RestoreReport(len(wanted), 0, 0, len(initial), 0.0)
@@ -228,7 +240,10 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
                 if p.kind == "bytes":
                     hslot.numpy()[off:off + p.nbytes] = np.frombuffer(
                         p.host, dtype=np.uint8)[p.host_off:p.host_off + p.nbytes]
-                    rep.storage_bytes += p.nbytes
+                    if p.entry is None and plan.decisions[p.unit].source == "memory":
+                        rep.memory_bytes += p.nbytes
+                    else:
+                        rep.storage_bytes += p.nbytes
             files_or_bytes = [(p, off) for p, off in batch if p.kind in ("file", "bytes")]
             for (p, _, _), c in zip(files, crcs):
                 prev = running.get(p.entry)
@@ -259,6 +274,9 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
             ring.free[slot] = t1
     torch.cuda.current_stream(dev).wait_stream(s)
     s.synchronize()
+    for peer in peers.values():
+        if peer is not None:
+            peer[0].close()
     rep.unpack_ms = sum(a.elapsed_time(b) for a, b, _ in timers)
     rep.batches = len(batches)
     rep.wall_s = time.perf_counter() - t_start

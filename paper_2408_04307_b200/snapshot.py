@@ -77,9 +77,12 @@ class DeviceCheckpointEngine(CheckpointEngine):
     def __init__(self, layout: RankLayout, store, arena: StateArena,
                  ranks: Optional[Sequence[int]] = None, n_buffers: int = 3,
                  pack_mode: int = D.MODE_AUTO, chunk_log2: int = D.DEFAULT_CHUNK_LOG2,
-                 control_group=None, persist_threads: int = 1):
+                 control_group=None, persist_threads: int = 1,
+                 shared_host_prefix: Optional[str] = None):
         import torch
         super().__init__(layout, store, n_buffers)
+        self.shared_prefix = shared_host_prefix
+        self._shared: Dict[int, object] = {}
         self.arena = arena
         self.device = arena.device
         self.ranks = tuple(ranks) if ranks is not None else arena.ranks
@@ -113,8 +116,78 @@ class DeviceCheckpointEngine(CheckpointEngine):
         import torch
         h = self.host[buffer_id]
         if h is None or h.numel() < nbytes:
-            self.host[buffer_id] = torch.empty(max(nbytes, 256), dtype=torch.uint8, pin_memory=True)
+            if self.shared_prefix is None:
+                self.host[buffer_id] = torch.empty(max(nbytes, 256), dtype=torch.uint8,
+                                                   pin_memory=True)
+            else:
+                from .hostmem import SharedHostBuffer, buffer_name
+                if len(self.ranks) != 1:
+                    raise ValueError("shared host buffers need one local rank per engine")
+                old = self._shared.pop(buffer_id, None)
+                self.host[buffer_id] = None
+                if old is not None:
+                    old.close()
+                shb = SharedHostBuffer(buffer_name(self.shared_prefix, self.ranks[0], buffer_id),
+                                       max(nbytes, 256))
+                self._shared[buffer_id] = shb
+                self.host[buffer_id] = shb.tensor
         return self.host[buffer_id]
+
+    # -- node-shared snapshot metadata (cross-process memory restore) ---------------
+    def _meta_path(self, rank: int, buffer_id: int) -> str:
+        from .hostmem import SHM_DIR, buffer_name
+        import os
+        return os.path.join(SHM_DIR, buffer_name(self.shared_prefix, rank, buffer_id) + ".json")
+
+    def _publish_meta(self, buf: Buffer, rec) -> None:
+        import json
+        import os
+        if self.shared_prefix is None:
+            return
+        for r in rec.layouts:
+            path = self._meta_path(r, buf.buffer_id)
+            tmp = path + ".tmp"
+            with open(tmp, "w") as f:
+                json.dump({"version": buf.version, "iteration": buf.iteration,
+                           "nbytes": rec.nbytes}, f)
+            os.replace(tmp, path)
+
+    def _retract_meta(self, buffer_id: int) -> None:
+        import os
+        if self.shared_prefix is None:
+            return
+        for r in self.ranks:
+            try:
+                os.unlink(self._meta_path(r, buffer_id))
+            except FileNotFoundError:
+                pass
+
+    def peer_buffer(self, rank: int, version: int):
+        """(host array, StagingLayout) of peer ``rank``'s in-memory copy of
+        ``version`` on this node, or None."""
+        import json
+        from .arena import PeerSlots
+        from .hostmem import SharedHostBuffer, buffer_name
+        if self.shared_prefix is None:
+            return None
+        buf = next((b for b in self.buffers.buffers if b.version == version), None)
+        if buf is None or buf.content is None:
+            return None
+        for bid in range(len(self.buffers.buffers)):
+            try:
+                with open(self._meta_path(rank, bid)) as f:
+                    meta = json.load(f)
+            except (FileNotFoundError, ValueError):
+                continue
+            if meta.get("version") != version:
+                continue
+            shb = SharedHostBuffer(buffer_name(self.shared_prefix, rank, bid), create=False,
+                                   register=False)
+            st = StagingLayout.build(buf.content.get(rank, ()), PeerSlots(self.layout, rank), rank)
+            if st.nbytes != meta["nbytes"]:
+                raise RuntimeError(f"peer rank {rank} v{version}: layout size mismatch")
+            return shb, st
+        return None
 
     def reserve(self, nbytes: int) -> None:
         """Pre-allocate staging and all host buffers (pinning is slow: do it
@@ -164,6 +237,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
                        assignment: PhaseAssignment, plan_key=None, compute_stream=None) -> Buffer:
         import torch
         buf = super().begin_snapshot(iteration, checkpoint_index, assignment)
+        self._retract_meta(buf.buffer_id)
         try:
             table, layouts, region, nbytes = self._table_for(assignment, plan_key)
             host = self._ensure_host(buf.buffer_id, nbytes)
@@ -245,6 +319,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
         from .planner import build_phase_assignment
         rank = self.ranks[0]
         buf = CheckpointEngine.begin_snapshot(self, iteration, checkpoint_index, None)
+        self._retract_meta(buf.buffer_id)
         compute = compute_stream or torch.cuda.current_stream(self.device)
         ps, cs, ms = self.pack_stream, self.copy_stream, self._meta_stream
         ps.wait_stream(compute)
@@ -307,6 +382,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
             rec.drain_done.synchronize()
             self.stats["pack_ms"].append(rec.pack_start.elapsed_time(rec.pack_done))
             self.stats["drain_ms"].append(rec.pack_done.elapsed_time(rec.drain_done))
+            self._publish_meta(buf, rec)
         return super().complete_snapshot(buf)
 
     # -- host bytes ---------------------------------------------------------------------
@@ -370,6 +446,11 @@ class DeviceCheckpointEngine(CheckpointEngine):
 
     def close(self) -> None:
         self._persist_pool.shutdown(wait=True)
+        for bid, shb in list(self._shared.items()):
+            self._retract_meta(bid)
+            self.host[bid] = None
+            shb.close()
+        self._shared.clear()
 
 
 class PecCheckpointer:
@@ -386,7 +467,7 @@ class PecCheckpointer:
                  strategy: str = EQUAL_PEC, i_ckpt: int = 10, ranks: Optional[Sequence[int]] = None,
                  counters=None, group=None, control_group=None, n_buffers: int = 3,
                  pack_mode: int = D.MODE_AUTO, chunk_log2: int = D.DEFAULT_CHUNK_LOG2,
-                 async_persist: bool = True):
+                 async_persist: bool = True, shared_host_prefix: Optional[str] = None):
         self.layout = layout
         self.arena = arena
         self.pec = pec
@@ -394,7 +475,8 @@ class PecCheckpointer:
         self.i_ckpt = i_ckpt
         self.group = group
         self.engine = DeviceCheckpointEngine(layout, store, arena, ranks, n_buffers, pack_mode,
-                                             chunk_log2, control_group)
+                                             chunk_log2, control_group,
+                                             shared_host_prefix=shared_host_prefix)
         self.counters = counters
         self.async_persist = async_persist
         self.persist_sel: Dict[int, Dict[int, frozenset]] = {}

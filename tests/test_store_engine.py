@@ -241,3 +241,30 @@ def test_fig7_two_level_recovery():
     assert d1["ew.L0.E3"].source == "initial"
     with pytest.raises(UnrecoverableStateError):
         CheckpointEngine(layout, MemoryStore()).resolve_recovery(set())
+
+
+def test_shared_host_buffer_visible_to_a_peer_mapping():
+    import uuid
+    from paper_2408_04307_b200.hostmem import SharedHostBuffer
+    name = f"pec_test_{uuid.uuid4().hex}"
+    owner = SharedHostBuffer(name, 1 << 16, create=True, register=False)
+    owner.array[100:110] = np.arange(10, dtype=np.uint8)
+    peer = SharedHostBuffer(name, create=False, register=False)
+    assert peer.nbytes == 1 << 16
+    assert bytes(peer.array[100:110]) == bytes(range(10))
+    peer.close()
+    owner.close()
+    import os
+    assert not os.path.exists(owner.path)
+
+
+def test_arena_slots_are_recomputable_for_peers():
+    from paper_2408_04307_b200.arena import PeerSlots, arena_slots
+    layout = make_layout(n_experts=4, dp=4, ep=2, epp=1001, other=13)
+    for r in range(4):
+        a = arena_slots(layout, [r])
+        assert PeerSlots(layout, r).slots == a
+        offs = sorted(s.offset for s in a.values())
+        assert all(o % 256 == 0 for o in offs)
+        ends = sorted((s.offset, s.offset + s.size) for s in a.values())
+        assert all(e0[1] <= e1[0] for e0, e1 in zip(ends, ends[1:]))

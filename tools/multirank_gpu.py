@@ -61,7 +61,10 @@ def main():
     dist.barrier()
 
     w = configs.gpt350m_16e(k_pec=2, strategy="equal_pec", dp=world, ep=world)
-    layout = w.layout()
+    # one rank per "node" so a node fault leaves peers whose host snapshot
+    # buffers (node-shared /dev/shm) serve memory-sourced restores
+    from paper_2408_04307_b200 import ClusterSpec, build_layout
+    layout = build_layout(w.model, w.parallel, ClusterSpec(num_nodes=world, gpus_per_node=1))
     L, E = layout.model.num_moe_layers, layout.model.experts_per_layer
     arena = StateArena(layout, [rank], dev, w.expert_tensors)
     routed = 4096 * 2
@@ -71,7 +74,7 @@ def main():
     store = DiskStore(root)
     ck = PecCheckpointer(layout, arena, store, pec, "equal_pec", i_ckpt=3, ranks=[rank],
                          counters=counters, group=None, control_group=control,
-                         async_persist=False)
+                         async_persist=False, shared_host_prefix="pec_mr")
     ck.group = dist.group.WORLD  # NCCL group for the counter all-reduce
 
     glob = np.zeros((2, L, E), dtype=np.int64)
@@ -116,23 +119,31 @@ def main():
         for k in mine:
             files_ok &= crc32c(data[k]) == persisted_bytes[v]["entries"][k]
     dist.barrier()
-    # storage restore of this rank's resident units that the newest version covers
-    plan = ck.engine.resolve_recovery({0}, max_iteration=None)  # node 0 (all ranks) failed
-    ck.engine.on_fault({0})
-    keys = [k for k, d in plan.decisions.items() if arena.has(k) and d.source == "storage"]
-    for k in keys:
-        arena.unit_bytes(k).zero_()
+    # node `world-1` fails: every rank restores all of its resident units from
+    # memory (own or a surviving peer's node-shared buffer), storage or initial
+    failed = {world - 1}
+    plan = ck.engine.resolve_recovery(failed)
+    ck.engine.on_fault(failed)
+    keys = [k for k in plan.decisions if arena.has(k)]
+    arena.buffer.zero_()
     rep = restore(ck.engine, plan, keys=keys)
     after = arena.buffer.cpu().numpy()
     restore_ok = bool(keys)
+    sources = {}
     for k in keys:
         d = plan.decisions[k]
+        sources[d.source] = sources.get(d.source, 0) + 1
         sl = arena.slot(k)
-        restore_ok &= crc32c(after[sl.offset:sl.offset + sl.size]) == persisted_bytes[d.version]["units"][k]
+        want = persisted_bytes[d.version]["units"][k] if d.source != "initial" else None
+        if want is not None:
+            restore_ok &= crc32c(after[sl.offset:sl.offset + sl.size]) == want
+    dist.barrier()  # peers may still be reading this rank's shared buffers
     ck.close()
     res = {"rank": rank, "world": world, "selection_ok": bool(sel_ok), "files_ok": bool(files_ok),
            "restore_ok": bool(restore_ok), "versions": versions, "restored_units": len(keys),
-           "restored_bytes": rep.storage_bytes, "seconds": round(time.time() - t0, 1)}
+           "sources": sources, "memory_bytes": rep.memory_bytes,
+           "storage_bytes": rep.storage_bytes, "restore_wall_s": round(rep.wall_s, 2),
+           "seconds": round(time.time() - t0, 1)}
     print(json.dumps(res), flush=True)
     dist.barrier()
     if rank == 0:
