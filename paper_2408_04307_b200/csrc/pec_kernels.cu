@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cub/block/block_scan.cuh>
+
 #include "pec.h"
 
 namespace {
@@ -498,56 +500,99 @@ copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
 // The template is the rank's entry list for "every expert due", in the
 // reference's order (planner.py:263-295: owned, experts by (layer, expert),
 // non-expert modules).  For any due set the rank's entries are the
-// subsequence whose (layer, expert) is selected (layer < 0: always kept), so
-// one warp filters the template against sel[L][K] and lays the kept entries
-// out in staging with the StagingLayout rule (offset >= previous end and
-// == source mod align), writing a ready pec_copy_desc table (dropped
-// entries: nbytes = 0) plus {total chunks, staged bytes}.
-__global__ void expand_plan_kernel(const pec_plan_template* __restrict__ tmpl, int n,
-                                   const int32_t* __restrict__ sel, int L, int K,
-                                   uint64_t state_base, uint64_t stage_base, int lg,
-                                   uint64_t align, pec_copy_desc* __restrict__ out,
-                                   uint64_t* __restrict__ totals) {
-  const int lane = threadIdx.x;
-  uint64_t pos = 0, chunks = 0;  // meaningful in lane 0
+// subsequence whose (layer, expert) is selected (layer < 0: always kept).
+//
+// Placement (the StagingLayout rule: offset >= previous end, == source mod
+// A) is a scan: every placed offset is == its source mod A, so the previous
+// kept entry ends at (s_prev + n_prev) mod A and entry i's pad is
+// (s_i - s_prev - n_prev) mod A — known without the absolute position.
+// Offsets are then an exclusive prefix sum of (pad + n), chunk starts a
+// prefix sum of ceil(n / 2^lg): one block, CUB block scans over tiles of
+// kExpandThreads entries with carries between tiles.
+constexpr int kExpandThreads = 512;
+
+struct PrevKept {  // scan element: index of the latest kept entry so far
+  __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
+};
+
+__global__ void __launch_bounds__(kExpandThreads)
+expand_plan_kernel(const pec_plan_template* __restrict__ tmpl, int n,
+                   const int32_t* __restrict__ sel, int L, int K,
+                   uint64_t state_base, uint64_t stage_base, int lg, uint64_t align,
+                   pec_copy_desc* __restrict__ out, uint64_t* __restrict__ totals) {
+  using ScanU = cub::BlockScan<unsigned long long, kExpandThreads>;
+  using ScanI = cub::BlockScan<int, kExpandThreads>;
+  __shared__ union {
+    typename ScanU::TempStorage u;
+    typename ScanI::TempStorage i;
+  } tmp;
+  __shared__ uint64_t end_mod[kExpandThreads];   // (s + n) mod A of kept entries in the tile
+  __shared__ unsigned long long carry_bytes, carry_chunks;
+  __shared__ uint64_t carry_end;                   // end mod A of the last kept entry so far
+  __shared__ int carry_any;
   const uint64_t span = 1ull << lg;
-  for (int base = 0; base < n; base += 32) {
-    const int i = base + lane;
-    bool keep = false;
-    if (i < n) {
-      const int layer = tmpl[i].layer;
-      if (layer < 0) {
-        keep = true;
-      } else if (layer < L) {
-        const int e = tmpl[i].expert;
-        for (int k = 0; k < K; ++k) keep |= (sel[(int64_t)layer * K + k] == e);
-      }
-    }
-    const unsigned kept = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) {
-      const int m = n - base < 32 ? n - base : 32;
-      for (int j = 0; j < m; ++j) {
-        const pec_plan_template t = tmpl[base + j];
-        pec_copy_desc dsc;
-        dsc.src = state_base + t.src_offset;
-        dsc.first_chunk = chunks;
-        if ((kept >> j) & 1u) {
-          const uint64_t off = pos + ((t.src_offset - pos) % align + align) % align;
-          dsc.dst = stage_base + off;
-          dsc.nbytes = t.nbytes;
-          pos = off + t.nbytes;
-          chunks += (t.nbytes + span - 1) / span;
-        } else {
-          dsc.dst = stage_base + pos;
-          dsc.nbytes = 0;
-        }
-        out[base + j] = dsc;
-      }
-    }
+  const uint64_t amask = align - 1;                // align is a power of two
+  if (threadIdx.x == 0) {
+    carry_bytes = 0;
+    carry_chunks = 0;
+    carry_end = 0;
+    carry_any = 0;
   }
-  if (lane == 0) {
-    totals[0] = chunks;
-    totals[1] = pos;
+  __syncthreads();
+  for (int base = 0; base < n; base += kExpandThreads) {
+    const int i = base + threadIdx.x;
+    bool keep = false;
+    uint64_t src = 0, nb = 0;
+    if (i < n) {
+      const pec_plan_template t = tmpl[i];
+      src = t.src_offset;
+      nb = t.nbytes;
+      if (t.layer < 0) {
+        keep = true;
+      } else if (t.layer < L) {
+        for (int k = 0; k < K; ++k) keep |= (sel[(int64_t)t.layer * K + k] == t.expert);
+      }
+    }
+    // previous kept entry inside this tile (or -1 -> carried end)
+    int prev = -1;
+    ScanI(tmp.i).ExclusiveScan(keep ? (int)threadIdx.x : -1, prev, -1, PrevKept());
+    end_mod[threadIdx.x] = (src + nb) & amask;
+    __syncthreads();
+    const uint64_t prev_end = prev >= 0 ? end_mod[prev] : (carry_any ? carry_end : 0);
+    const uint64_t pad = keep ? ((src - prev_end) & amask) : 0;
+    const unsigned long long size = keep ? (unsigned long long)(pad + nb) : 0ull;
+    const unsigned long long nch = keep ? (unsigned long long)((nb + span - 1) / span) : 0ull;
+    unsigned long long pos_before = 0, tile_bytes = 0;
+    ScanU(tmp.u).ExclusiveSum(size, pos_before, tile_bytes);
+    __syncthreads();
+    unsigned long long ch_before = 0, tile_chunks = 0;
+    ScanU(tmp.u).ExclusiveSum(nch, ch_before, tile_chunks);
+    if (i < n) {
+      pec_copy_desc d;
+      d.src = state_base + src;
+      d.first_chunk = carry_chunks + ch_before;
+      const uint64_t off = carry_bytes + pos_before + pad;
+      d.dst = stage_base + (keep ? off : carry_bytes + pos_before);
+      d.nbytes = keep ? nb : 0;
+      out[i] = d;
+    }
+    // the last thread's inclusive "latest kept" index is the tile's last kept entry
+    __shared__ int tile_last;
+    if (threadIdx.x == kExpandThreads - 1) tile_last = keep ? (int)threadIdx.x : prev;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (tile_last >= 0) {
+        carry_end = end_mod[tile_last];
+        carry_any = 1;
+      }
+      carry_bytes += tile_bytes;
+      carry_chunks += tile_chunks;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    totals[0] = carry_chunks;
+    totals[1] = carry_bytes;
   }
 }
 
@@ -692,8 +737,9 @@ int pec_expand_plan(const pec_plan_template* tmpl, int n, const int32_t* sel, in
   if (n < 0 || L < 1 || K < 1 || chunk_log2 < 12 || chunk_log2 > 24 || stage_align < 1) return PEC_E_INVAL;
   if (n > 0 && (tmpl == nullptr || out == nullptr)) return PEC_E_INVAL;
   if (sel == nullptr || totals == nullptr) return PEC_E_INVAL;
-  expand_plan_kernel<<<1, 32, 0, as_stream(stream)>>>(tmpl, n, sel, L, K, state_base, stage_base,
-                                                      chunk_log2, (uint64_t)stage_align, out, totals);
+  if (stage_align & (stage_align - 1)) return PEC_E_INVAL;
+  expand_plan_kernel<<<1, kExpandThreads, 0, as_stream(stream)>>>(
+      tmpl, n, sel, L, K, state_base, stage_base, chunk_log2, (uint64_t)stage_align, out, totals);
   return launch_status();
 }
 

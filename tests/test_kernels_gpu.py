@@ -206,21 +206,28 @@ def test_pack_plan_phases_bit_exact(dev, mode):
                 assert st.payload_bytes == plan.workload_bytes[plan.assignments.index(phase)][rank]
 
 
-@pytest.mark.parametrize("strategy", ["equal_pec", "baseline"])
-def test_device_plan_expansion_matches_host_plan(dev, strategy):
+@pytest.mark.parametrize("strategy,shape", [("equal_pec", "split"), ("baseline", "split"),
+                                            ("equal_pec", "many")])
+def test_device_plan_expansion_matches_host_plan(dev, strategy, shape):
     """pec_expand_plan + pec_pack_indirect == host build_phase_assignment +
     StagingLayout + oracle pack, for random selections on a 2-EP-group layout
-    (byte-split expert weights), every rank."""
+    (byte-split expert weights, every rank) and on a 64-expert layout whose
+    template spans several scan tiles."""
     import torch
     from paper_2408_04307_b200 import build_phase_assignment
     from paper_2408_04307_b200 import device as D
     from paper_2408_04307_b200.arena import StateArena
     from paper_2408_04307_b200.staging import PlanTemplate, StagingLayout
-    layout = make_layout(n_experts=8, dp=4, ep=2, n_layers=3, epp=20_001, p_ne=3_001, other=9,
-                         modules=(("a", 1000), ("b", 1001), ("c", 1000)))
-    L, E = 3, 8
+    if shape == "split":
+        layout = make_layout(n_experts=8, dp=4, ep=2, n_layers=3, epp=20_001, p_ne=3_001,
+                             other=9, modules=(("a", 1000), ("b", 1001), ("c", 1000)))
+        L, E, ranks = 3, 8, range(4)
+    else:
+        layout = make_layout(n_experts=64, dp=1, ep=1, gpus_per_node=1, n_layers=12, epp=333,
+                             p_ne=3_001, modules=(("a", 1000), ("b", 1001), ("c", 1000)))
+        L, E, ranks = 12, 64, range(1)
     rng = np.random.default_rng(7)
-    for rank in range(4):
+    for rank in ranks:
         arena = StateArena(layout, [rank], dev)
         host_state = arena.buffer.cpu().numpy()
         tmpl = PlanTemplate(layout, arena, rank, strategy, dev)
