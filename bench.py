@@ -309,8 +309,10 @@ def run_reference(args):
             "ms_per_step": round(sample * 1e9 / (value * 1e9) * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": w.name, "rank": 0, "plan": w.strategy,
-                       "k_pec": w.pec.k_pec, "sample_gb": round(sample, 3)},
+            "config": {"workload": w.name, "plan": w.strategy, "selection": w.pec.selection,
+                       "k_pec": w.pec.k_pec, "ranks": f"0 of dp={layout.n_ranks} (host cores)",
+                       "parallelism": f"dp{layout.n_ranks}-ep{layout.parallel.ep_degree}",
+                       "sample_gb": round(sample, 3)},
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads,
                              "kind": "port", "sample": desc},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -368,7 +370,6 @@ def run_b200(args):
     pt = getattr(eng, "template", None)
     la_bytes = None
     if plan is None:
-        from paper_2408_04307_b200.selector import select_window as _sw
         # payload of the load-aware steps: measured from the host mirror of
         # each step's selection after the timed region
         la_bytes = []
@@ -413,7 +414,6 @@ def run_b200(args):
     pack_ms = [a.elapsed_time(b) for a, b in evs]
     if plan is None:
         # bytes of each load-aware step from the host mirror of its selection
-        from paper_2408_04307_b200.staging import StagingLayout as _SL
         sels = la_bytes[-args.steps:]
         moved = 0
         for sd in sels:

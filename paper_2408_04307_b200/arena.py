@@ -27,17 +27,9 @@ source of `engine.resolve_recovery` can be regenerated bit-identically.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Dict, Iterable, List, Optional, Sequence, Tuple
+from typing import Dict, Iterable, Optional, Sequence, Tuple
 
-from .topology import (
-    EXPERT_OPTIM,
-    EXPERT_WEIGHT,
-    NON_EXPERT_OPTIM,
-    NON_EXPERT_WEIGHT,
-    OTHER_STATES,
-    RankLayout,
-    StateUnit,
-)
+from .topology import EXPERT_OPTIM, EXPERT_WEIGHT, NON_EXPERT_WEIGHT, RankLayout
 
 ARENA_ALIGN = 256
 BASE_SEED = 7  # default make_scenario seed (reference tests/test_simulator.py:26)

@@ -18,7 +18,7 @@ The payload never crosses GPUs; only two small exchanges exist
 
 from __future__ import annotations
 
-from typing import Callable, Iterable, List, Mapping, Optional, Sequence, Tuple
+from typing import Callable, Iterable, List, Mapping, Optional, Sequence
 
 from .store import StoreEntry
 

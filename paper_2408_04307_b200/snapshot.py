@@ -29,11 +29,10 @@ token counting every iteration, selection + plan + snapshot every
 
 from __future__ import annotations
 
-import threading
 import time
 from concurrent.futures import Future, ThreadPoolExecutor
-from dataclasses import dataclass, field
-from typing import Dict, Iterable, List, Mapping, Optional, Sequence, Tuple
+from dataclasses import dataclass
+from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -43,7 +42,6 @@ from .engine import Buffer, CheckpointEngine, NoFreeBufferError
 from .planner import (
     ADAPTIVE_PEC,
     BASELINE,
-    EQUAL_FULL,
     EQUAL_PEC,
     LOAD_AWARE,
     PecConfig,
