@@ -49,8 +49,10 @@ def global_two_tier_select(local_counts, k_snapshot: int, k_persist: int,
 
 def commit_version(store, version: int, iteration: int, checkpoint_index: int,
                    entries: Sequence[StoreEntry], local_ranks: Iterable[int],
-                   payloads: Optional[Mapping[str, object]], group=None) -> None:
-    """Write this process's entries, then publish the version once."""
+                   payloads: Optional[Mapping[str, object]], group=None,
+                   before_publish: Optional[Callable[[], None]] = None) -> None:
+    """Write this process's entries, then publish the version once.
+    ``before_publish`` may raise to abandon the version (no COMPLETE)."""
     import torch.distributed as dist
     local = set(local_ranks)
     mine = [e for e in entries if e.rank in local]
@@ -58,12 +60,22 @@ def commit_version(store, version: int, iteration: int, checkpoint_index: int,
     if world == 1:
         store.check_version(version)
         rows = store.write_entries(version, iteration, mine, payloads=payloads)
+        if before_publish is not None:
+            before_publish()
         store.publish(version, iteration, checkpoint_index, entries, rows)
         return
     rows = store.write_entries(version, iteration, mine, payloads=payloads)
     gathered: List[Optional[list]] = [None] * world
     dist.all_gather_object(gathered, rows, group=group)
+    err = None
     if dist.get_rank(group) == 0:
-        store.publish(version, iteration, checkpoint_index, entries,
-                      [r for part in gathered for r in part])
-    dist.barrier(group=group)
+        try:
+            if before_publish is not None:
+                before_publish()
+            store.publish(version, iteration, checkpoint_index, entries,
+                          [r for part in gathered for r in part])
+        except Exception as e:  # noqa: BLE001 - re-raised after the barrier
+            err = e
+    dist.barrier(group=group)  # every rank leaves, published or not
+    if err is not None:
+        raise err

@@ -29,6 +29,7 @@ token counting every iteration, selection + plan + snapshot every
 
 from __future__ import annotations
 
+import threading
 import time
 from concurrent.futures import Future, ThreadPoolExecutor
 from dataclasses import dataclass
@@ -56,6 +57,10 @@ from .selector import select_window
 from .staging import DeviceTable, PlanTemplate, StagingLayout
 from .store import StoreEntry
 from .topology import RankLayout
+
+
+class PersistAborted(RuntimeError):
+    """A fault interrupted a persist before its version was published."""
 
 
 @dataclass
@@ -97,6 +102,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
         self._persist_pool = ThreadPoolExecutor(max_workers=persist_threads,
                                                 thread_name_prefix="pec-persist")
         self._persist: Dict[int, Tuple[Future, List[StoreEntry]]] = {}
+        self._abort_persist = threading.Event()
         self.stats = {"pack_ms": [], "drain_ms": [], "persist_s": [], "snap_bytes": []}
 
     # -- buffers -----------------------------------------------------------------
@@ -406,8 +412,14 @@ class DeviceCheckpointEngine(CheckpointEngine):
         from .distributed import commit_version
         t0 = time.perf_counter()
         local = [e for e in entries if e.rank in self.ranks]
+
+        def abort_check():
+            if self._abort_persist.is_set():
+                raise PersistAborted(f"persist of v{buf.version} aborted by a fault")
+
         commit_version(self.store, buf.version, buf.iteration, buf.checkpoint_index, entries,
-                       self.ranks, self.payloads(buf, local), group=self.group)
+                       self.ranks, self.payloads(buf, local), group=self.group,
+                       before_publish=abort_check)
         return time.perf_counter() - t0
 
     def start_persist(self, buf: Buffer, entries: List[StoreEntry]) -> Future:
@@ -434,12 +446,25 @@ class DeviceCheckpointEngine(CheckpointEngine):
         return self.buffers.complete_persist(buf)
 
     def on_fault(self, failed_nodes: Iterable[int]) -> None:
-        for fut, _ in self._persist.values():
+        """Reference semantics (engine.py:200-212) with real work in flight:
+        the in-flight pack/drain is allowed to land (its buffer is then
+        cleared, so nothing can reuse it while the copy engine still writes
+        it), and an in-flight persist is aborted before it publishes — a
+        torn version has no COMPLETE marker and is ignored by readers."""
+        self.pack_stream.synchronize()
+        self.copy_stream.synchronize()
+        self._abort_persist.set()
+        published = []
+        for bid, (fut, _) in self._persist.items():
             try:
-                fut.result()
-            except Exception:  # noqa: BLE001 - an interrupted persist leaves no version
+                self.stats["persist_s"].append(fut.result())
+                published.append(bid)   # it won the race: the version is COMPLETE
+            except PersistAborted:
                 pass
         self._persist.clear()
+        self._abort_persist.clear()
+        for bid in published:
+            self.buffers.complete_persist(self.buffers.buffers[bid])
         super().on_fault(failed_nodes)
 
     def close(self) -> None:
@@ -592,6 +617,15 @@ class PecCheckpointer:
         buf, persist_due = self.engine.begin_snapshot_device(iteration, c, snap_d, pers_d)
         self.persist_sel[buf.version] = persist_due
         return buf
+
+    def on_fault(self, failed_nodes) -> None:
+        """Engine fault handling, then resume an interrupted persist
+        (simulator.py:511-525)."""
+        self.engine.on_fault(failed_nodes)
+        if self.engine.buffers.persisting is None:
+            nxt = self.engine.buffers.promote_if_idle()
+            if nxt is not None:
+                self._start_persist(nxt)
 
     def wait_pack(self, stream=None) -> None:
         self.engine.wait_pack(stream=stream)

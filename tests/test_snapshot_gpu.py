@@ -186,3 +186,42 @@ def test_gpt350m_k_sweep_pack_bit_exact_on_device(dev, k):
             assert st.payload_bytes == plan.workload_bytes[phase_idx][r]
     del arena
     torch.cuda.empty_cache()
+
+
+def test_fault_mid_snapshot_and_mid_persist_leaves_consistent_state(dev, tmp_path):
+    """A fault while a snapshot drains discards it (its buffer is only freed
+    after the copy engine finished), a fault while persisting publishes no
+    version; later checkpoints and recovery are unaffected."""
+    import torch
+    from paper_2408_04307_b200 import configs
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.engine import FREE, SNAPSHOTTED
+    from paper_2408_04307_b200.restore import restore
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore
+    w = configs.toy()
+    layout = w.layout()
+    arena = StateArena(layout, [0], dev, w.expert_tensors)
+    store = DiskStore(tmp_path)
+    ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=1)
+    b1 = ck.step(1)                    # snapshotting
+    ck.engine.on_fault(set())          # fault before the drain is observed
+    assert b1.status == FREE
+    ck.hold_persist(True)
+    b2 = ck.step(2)
+    ck._complete(b2)                   # SNAPSHOTTED -> PERSISTING, held (not started)
+    ck.hold_persist(False)             # persist starts in the background ...
+    ck.engine.on_fault(set())          # ... and is aborted before publishing (or won)
+    assert store.complete_versions() in ([], [b2.version])
+    assert b2.status == (SNAPSHOTTED if not store.complete_versions() else "recovery")
+    ck.on_fault(set())                 # resumes the interrupted persist, if any
+    torch.cuda.synchronize()
+    good = arena.buffer.cpu().numpy().copy()
+    b3 = ck.step(3)
+    ck.finish()
+    assert b3.version in store.complete_versions()
+    plan = ck.engine.resolve_recovery(set())
+    arena.buffer.zero_()
+    restore(ck.engine, plan)
+    assert np.array_equal(arena.buffer.cpu().numpy(), good)
+    ck.close()
