@@ -317,11 +317,55 @@ def gen_recovery():
     return {"cases": cases}
 
 
+def gen_policy():
+    """Reference adaptive_configure / analytic_overhead on a grid."""
+    from mocsim import adaptive_configure, analytic_overhead
+    from mocsim.planner import PecConfig as RPec
+    cases = []
+    rng = random.Random(740)
+    specs = [("gpt350m", configs.gpt350m_16e(k_pec=2)), ("toy", configs.toy()),
+             ("mixtral", configs.mixtral_8x7b())]
+    for name, w in specs:
+        model = ref_model(w.model)
+        for strategy in ("equal_pec", "adaptive_pec"):
+            for _ in range(4):
+                snap_bw = 10 ** rng.uniform(8.5, 12.5)
+                pers_bw = 10 ** rng.uniform(8, 10.5)
+                fb = rng.choice([0.05, 0.3, 1.0])
+                upd = rng.choice([0.01, 0.05])
+                target = rng.choice([None, 1.0, 10.0, 60.0])
+                cl = mocsim.ClusterSpec(num_nodes=w.cluster.num_nodes,
+                                        gpus_per_node=w.cluster.gpus_per_node,
+                                        snapshot_bandwidth=snap_bw, persist_bandwidth=pers_bw,
+                                        fb_time=fb, update_time=upd, restart_time=1.0)
+                sc = Scenario(model=model, parallel=mocsim.ParallelSpec(w.parallel.dp_degree,
+                                                                        w.parallel.ep_degree),
+                              cluster=cl, strategy=strategy, i_ckpt=1, i_total=10, rng_seed=7,
+                              tokens_per_iteration=100, pec=RPec(k_pec=1))
+                cfg = adaptive_configure(sc, persist_target_s=target)
+                cases.append({"workload": name, "strategy": strategy, "snapshot_bw": snap_bw,
+                              "persist_bw": pers_bw, "fb": fb, "update": upd, "target": target,
+                              "k_snapshot": cfg.pec.k_snapshot, "k_persist": cfg.pec.k_persist,
+                              "i_ckpt": cfg.i_ckpt, "overlapped": cfg.snapshot_overlapped,
+                              "target_met": cfg.persist_target_met})
+    ana = []
+    for _ in range(50):
+        kw = dict(o_save_full_us=rng.uniform(1e3, 1e7), i_ckpt_full=rng.randint(1, 100),
+                  o_save_moc_us=rng.uniform(1e2, 1e6), i_ckpt_moc=rng.randint(1, 100),
+                  iter_time_us=rng.uniform(1e4, 1e7), failure_rate=rng.uniform(0, 0.01),
+                  o_restart_us=rng.uniform(1e5, 1e8), i_total=rng.randint(100, 100000))
+        r = analytic_overhead(**kw)
+        ana.append({"args": kw, "full": r.o_ckpt_full_us, "moc": r.o_ckpt_moc_us,
+                    "wins": r.moc_wins})
+    return {"configure": cases, "analytic": ana}
+
+
 def main():
     HERE.mkdir(exist_ok=True)
     for name, fn in [("routing", gen_routing), ("selection", gen_selection),
                      ("loadaware_sim", gen_loadaware_sim), ("plans", gen_plans),
-                     ("store", gen_store), ("recovery", gen_recovery)]:
+                     ("store", gen_store), ("recovery", gen_recovery),
+                     ("policy", gen_policy)]:
         doc = fn()
         doc["_generated_by"] = "tests/golden/make_golden.py (reference mocsim 0.1.0)"
         (HERE / f"{name}.json").write_text(json.dumps(doc, indent=None, sort_keys=True) + "\n")
