@@ -355,7 +355,7 @@ def run_b200(args):
     if world > 1 and store is not None:
         import torch.distributed as dist
         control = dist.new_group(backend="gloo")
-    mode = {"vec": D.MODE_VEC, "bulk": D.MODE_BULK}[args.engine]
+    mode = {"vec": D.MODE_VEC, "bulk": D.MODE_BULK, "crc": D.MODE_CRC}[args.engine]
     ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=1, ranks=[rank],
                          counters=counters, control_group=control, pack_mode=mode,
                          chunk_log2=args.chunk_log2)
@@ -587,7 +587,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="mixtral", choices=["toy", "gpt125m", "gpt350m", "mixtral"])
-    ap.add_argument("--engine", default="bulk", choices=["vec", "bulk"])
+    ap.add_argument("--engine", default="bulk", choices=["vec", "bulk", "crc"],
+                    help="pack engine: TMA bulk (default), LDG/STG vector, or vector with "
+                         "fused per-entry CRC-32C")
     ap.add_argument("--chunk-log2", type=int, default=15)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--persist", default="auto", choices=["auto", "none", "shm", "disk"])

@@ -135,6 +135,19 @@ int pec_expand_plan(const pec_plan_template* tmpl, int n, const int32_t* sel, in
 int pec_pack_indirect(const pec_copy_desc* descs, int n, uint64_t max_chunks,
                       const uint64_t* total_chunks_dev, int chunk_log2, int mode, void* stream);
 
+/* ---- pack with fused CRC-32C ------------------ *
+ * Replaces: the host CRC of every persisted entry (store.crc32c,
+ * store.py:49-70, used for the manifest at store.py:213-216).
+ * Same copy as pec_pack (vectorised engine) and, in the same pass over the
+ * bytes, entry_crc[i] = CRC-32C of descriptor i's nbytes (== pec_crc32c of
+ * the staged entry).  chunk_log2 must be 15; chunk_crc is device scratch of
+ * total_chunks uint32; entry_crc is device memory of n uint32.
+ * total_chunks_dev (nullable) caps the chunk count from device memory, as in
+ * pec_pack_indirect (device-expanded plans). */
+int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
+                 const uint64_t* total_chunks_dev, int chunk_log2, uint32_t* chunk_crc,
+                 uint32_t* entry_crc, void* stream);
+
 /* Host helper: fill first_chunk of a HOST table in place and return the
  * total chunk count (negative PEC_E_* on bad input). */
 int64_t pec_plan_chunks(pec_copy_desc* host_descs, int n, int chunk_log2);

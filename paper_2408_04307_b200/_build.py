@@ -16,8 +16,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "libpec.so"
-SOURCES = [CSRC / "pec_kernels.cu", CSRC / "pec_host.cpp"]
-HEADERS = [ROOT / "include" / "pec.h"]
+SOURCES = [CSRC / "pec_kernels.cu", CSRC / "pec_crc.cu", CSRC / "pec_host.cpp"]
+HEADERS = [ROOT / "include" / "pec.h", CSRC / "pec_device.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB_PATH
     LIB_DIR.mkdir(parents=True, exist_ok=True)
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"),
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(CSRC),
            *map(str, SOURCES), "-o", str(tmp)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -1,0 +1,327 @@
+// pec_crc.cu — CRC-32C of every staged entry, computed by the pack itself.
+//
+// the persist tier checksums each entry
+// (store.crc32c, pkg/src/mocsim/store.py:49-70; the manifest column of
+// store.py:149-164).  Here the pack kernel checksums the bytes it already
+// holds in registers on their way from the state arena to the staging
+// buffer, so the host never reads the payload for CRC and the HBM traffic of
+// the pack is unchanged.
+//
+// CRC-32C is linear over GF(2): for the register form R (initial value 0,
+// no final inversion), R(A || B) = R(A) * x^(8|B|) mod P  ^  R(B), and the
+// standard CRC is crc(M) = ~(R(M) ^ ~0 * x^(8|M|) mod P).  So:
+//   pack_crc_kernel   each thread copies 128 contiguous bytes of a 32 KiB
+//                     chunk and folds them with a byte table kept in shared
+//                     memory once per lane (entry e of lane l at word
+//                     32e + l: every lookup of a warp hits 32 distinct
+//                     banks), then a warp shuffle tree and a cross-warp fold
+//                     combine the 256 partial registers with constant
+//                     shifts -> one register per chunk;
+//   crc_fold_kernel   one thread per chunk shifts its register by the bytes
+//                     that follow it in its entry and XORs it into the
+//                     entry's register (XOR is associative/commutative);
+//   crc_final_kernel  applies the initial value / final inversion per entry.
+// Multiplication mod P (reflected, bit 31 = x^0) is the shift-and-add
+// schoolbook product; x^(2^k) are precomputed on the host.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pec.h"
+#include "pec_device.cuh"
+
+namespace {
+
+using pecdev::as_stream;
+using pecdev::find_desc;
+using pecdev::launch_status;
+using pecdev::sm_count;
+
+constexpr uint32_t kPoly = 0x82F63B78u;
+constexpr int kCrcThreads = 256;
+constexpr int kCrcLg = 15;                            // 32 KiB chunks
+constexpr int kPerThread = (1 << kCrcLg) / kCrcThreads;  // 128 contiguous bytes
+constexpr int kVecPerThread = kPerThread / 16;        // 8 x 16 B
+constexpr int kTableWords = 256 * 32;                 // lane-replicated byte table
+
+// Constant multipliers, applied through 4-bit windows: mul(a, b) =
+// XOR_p N_a[p][(b >> 4p) & 15] with N_a[p][v] = a * (v << 4p): 8 shared-memory
+// lookups instead of a 32-step schoolbook product.
+constexpr int kNumMul = 9;  // S32, lane levels 128..2048 B, warp levels 4..16 KiB
+constexpr int kMulWords = kNumMul * 8 * 16;
+
+struct CrcConsts {
+  uint32_t x2k[64];         // x^(2^k) mod P
+  uint32_t mul[kNumMul];    // x^(8*32), x^(8*128*2^j) j<5, x^(8*4096*2^j) j<3
+};
+
+__host__ __device__ __forceinline__ uint32_t gf2_mul(uint32_t a, uint32_t b) {
+  uint32_t p = 0;
+#pragma unroll 8
+  for (int i = 31; i >= 0; --i) {
+    p ^= b & (0u - ((a >> i) & 1u));
+    b = (b >> 1) ^ (kPoly & (0u - (b & 1u)));
+  }
+  return p;
+}
+
+__device__ __forceinline__ uint32_t xpow_bytes(const uint32_t* x2k, uint64_t nbytes) {
+  uint32_t acc = 1u << 31;  // 1
+  int k = 3;                // 8 bits per byte
+  while (nbytes) {
+    if (nbytes & 1u) acc = gf2_mul(x2k[k], acc);
+    nbytes >>= 1;
+    ++k;
+  }
+  return acc;
+}
+
+__device__ __forceinline__ uint32_t shift_bytes(const uint32_t* x2k, uint32_t r, uint64_t n) {
+  return n ? gf2_mul(xpow_bytes(x2k, n), r) : r;
+}
+
+__device__ __forceinline__ int4 ld_cached(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
+  asm volatile("st.global.cs.v4.s32 [%0], {%1, %2, %3, %4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+__device__ __forceinline__ uint32_t fold_word(const uint32_t* tab, uint32_t c, uint32_t w) {
+  c ^= w;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) c = tab[(c & 0xFFu) << 5] ^ (c >> 8);
+  return c;
+}
+
+__device__ __forceinline__ uint32_t mul_const(const uint32_t* nib, uint32_t b) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) r ^= nib[p * 16 + ((b >> (4 * p)) & 15u)];
+  return r;
+}
+
+__global__ void __launch_bounds__(kCrcThreads, 2)
+pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
+                const uint64_t* __restrict__ total_dev, CrcConsts k,
+                uint32_t* __restrict__ chunk_raw) {
+  // dynamic smem: byte table | nibble tables | per-warp 4 KiB transpose tiles
+  extern __shared__ __align__(16) uint32_t table[];
+  uint32_t* nib = table + kTableWords;
+  uint32_t* stage = table + kTableWords + kMulWords;
+  __shared__ uint32_t warp_raw[kCrcThreads / 32];
+  __shared__ uint32_t warp_len[kCrcThreads / 32];
+  if (total_dev != nullptr) {
+    const uint64_t td = *total_dev;
+    total = td < total ? td : total;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < kTableWords; idx += kCrcThreads) {
+    uint32_t c = (uint32_t)(idx >> 5);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) c = (c & 1u) ? (c >> 1) ^ kPoly : c >> 1;
+    table[idx] = c;
+  }
+  for (int idx = tid; idx < kMulWords; idx += kCrcThreads) {
+    const int m = idx >> 7, p = (idx >> 4) & 7, v = idx & 15;
+    nib[idx] = gf2_mul(k.mul[m], (uint32_t)v << (4 * p));
+  }
+  __syncthreads();
+  const uint32_t* tab = table + lane;
+  const uint32_t* s32 = nib;                 // x^(8*32)
+  const uint32_t* lvl = nib + 128;           // lane tree levels, 128 words each
+  const uint32_t* wlv = nib + 6 * 128;       // warp tree levels
+
+  for (uint64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
+    const int i = find_desc(d, n, ch);
+    const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << kCrcLg;
+    const uint64_t nb = __ldg(&d[i].nbytes);
+    const uint64_t span = 1ull << kCrcLg;
+    const uint64_t len = off >= nb ? 0 : (nb - off < span ? nb - off : span);
+    const uint8_t* s = reinterpret_cast<const uint8_t*>(__ldg(&d[i].src) + off);
+    uint8_t* t = reinterpret_cast<uint8_t*>(__ldg(&d[i].dst) + off);
+    const bool fast = len == span && ((reinterpret_cast<uintptr_t>(s) |
+                                      reinterpret_cast<uintptr_t>(t)) & 15u) == 0;
+    uint32_t c = 0;
+    uint32_t my_len;
+    if (fast) {
+      // Coalesced: lane l of warp w moves 16-byte units l + 32k of the warp's
+      // 4 KiB (global -> registers -> staging), and parks them in a swizzled
+      // per-warp shared tile; then each lane reads back ITS contiguous 128 B
+      // (units 8l..8l+7) conflict-free and folds them as four independent
+      // 32-byte CRC chains.  Swizzle: unit u lives at 16-byte slot
+      // u ^ ((u >> 3) & 7), so both access patterns hit 8 distinct 16-byte
+      // bank groups per 8 lanes.
+      const int4* vs = reinterpret_cast<const int4*>(s) + warp * 256;
+      int4* vt = reinterpret_cast<int4*>(t) + warp * 256;
+      int4* tile = reinterpret_cast<int4*>(stage) + warp * 256;
+      int4 r[kVecPerThread];
+#pragma unroll
+      for (int u = 0; u < kVecPerThread; ++u) r[u] = __ldg(vs + lane + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kVecPerThread; ++u) {
+        __stcs(vt + lane + 32 * u, r[u]);
+        const int unit = lane + 32 * u;
+        tile[unit ^ ((unit >> 3) & 7)] = r[u];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < kVecPerThread; ++j) {
+        const int unit = lane * kVecPerThread + j;
+        r[j] = tile[unit ^ ((unit >> 3) & 7)];
+      }
+      uint32_t q[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+#pragma unroll
+          for (int ch4 = 0; ch4 < 4; ++ch4) {
+            const int4 v = r[ch4 * 2 + u];
+            const uint32_t word = w == 0 ? (uint32_t)v.x : w == 1 ? (uint32_t)v.y
+                                : w == 2 ? (uint32_t)v.z : (uint32_t)v.w;
+            q[ch4] = fold_word(tab, q[ch4], word);
+          }
+        }
+      }
+      __syncwarp();  // the tile is rewritten by the next chunk
+      c = mul_const(s32, mul_const(s32, mul_const(s32, q[0]) ^ q[1]) ^ q[2]) ^ q[3];
+      my_len = kPerThread;
+    } else {
+      // general chunk (unaligned head, partial tail): bytes, still 128 per thread
+      const uint64_t lo = (uint64_t)tid * kPerThread;
+      const uint64_t hi = lo + kPerThread < len ? lo + kPerThread : len;
+      for (uint64_t b = lo; b < hi; ++b) {
+        const uint8_t v = s[b];
+        t[b] = v;
+        c = tab[((c ^ v) & 0xFFu) << 5] ^ (c >> 8);
+      }
+      my_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
+    }
+    // warp tree: lanes hold consecutive pieces; fold right neighbours in
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const uint32_t oc = __shfl_down_sync(0xffffffffu, c, 1 << j);
+      const uint32_t ol = __shfl_down_sync(0xffffffffu, my_len, 1 << j);
+      if ((lane & ((2 << j) - 1)) == 0) {
+        c = (fast ? mul_const(lvl + j * 128, c) : shift_bytes(k.x2k, c, ol)) ^ oc;
+        my_len += ol;
+      }
+    }
+    if (lane == 0) {
+      warp_raw[warp] = c;
+      warp_len[warp] = my_len;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // cross-warp tree over the 8 warp registers (lanes 0..7)
+      uint32_t a = lane < kCrcThreads / 32 ? warp_raw[lane] : 0u;
+      uint32_t al = lane < kCrcThreads / 32 ? warp_len[lane] : 0u;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const uint32_t oc = __shfl_down_sync(0xffffffffu, a, 1 << j);
+        const uint32_t ol = __shfl_down_sync(0xffffffffu, al, 1 << j);
+        if ((lane & ((2 << j) - 1)) == 0) {
+          a = (fast ? mul_const(wlv + j * 128, a) : shift_bytes(k.x2k, a, ol)) ^ oc;
+          al += ol;
+        }
+      }
+      if (lane == 0) chunk_raw[ch] = a;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
+                                const uint64_t* __restrict__ total_dev, CrcConsts k,
+                                const uint32_t* __restrict__ chunk_raw,
+                                uint32_t* __restrict__ entry_raw) {
+  if (total_dev != nullptr) {
+    const uint64_t td = *total_dev;
+    total = td < total ? td : total;
+  }
+  __shared__ uint32_t x2k[64];
+  if (threadIdx.x < 64) x2k[threadIdx.x] = k.x2k[threadIdx.x];
+  __syncthreads();
+  for (uint64_t ch = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < total;
+       ch += (uint64_t)gridDim.x * blockDim.x) {
+    const int i = find_desc(d, n, ch);
+    const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << kCrcLg;
+    const uint64_t nb = __ldg(&d[i].nbytes);
+    if (off >= nb) continue;
+    const uint64_t end = off + (1ull << kCrcLg) < nb ? off + (1ull << kCrcLg) : nb;
+    atomicXor(&entry_raw[i], shift_bytes(x2k, chunk_raw[ch], nb - end));
+  }
+}
+
+__global__ void crc_final_kernel(const pec_copy_desc* __restrict__ d, int n, CrcConsts k,
+                                 uint32_t* __restrict__ entry) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t nb = d[i].nbytes;
+    entry[i] = nb ? ~(entry[i] ^ shift_bytes(k.x2k, 0xFFFFFFFFu, nb)) : 0u;
+  }
+}
+
+CrcConsts make_consts() {
+  CrcConsts k;
+  uint32_t p = 1u << 30;  // x^1
+  for (int i = 0; i < 64; ++i) {
+    k.x2k[i] = p;
+    p = gf2_mul(p, p);
+  }
+  auto xpow = [&](uint64_t nbytes) {
+    uint32_t acc = 1u << 31;
+    int b = 3;
+    while (nbytes) {
+      if (nbytes & 1u) acc = gf2_mul(k.x2k[b], acc);
+      nbytes >>= 1;
+      ++b;
+    }
+    return acc;
+  };
+  k.mul[0] = xpow(32);
+  for (int j = 0; j < 5; ++j) k.mul[1 + j] = xpow((uint64_t)kPerThread << j);
+  for (int j = 0; j < 3; ++j) k.mul[6 + j] = xpow((uint64_t)kPerThread * 32 << j);
+  return k;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
+                 const uint64_t* total_chunks_dev, int chunk_log2, uint32_t* chunk_crc,
+                 uint32_t* entry_crc, void* stream) {
+  if (chunk_log2 != kCrcLg || n < 0) return PEC_E_INVAL;
+  if (n == 0) return PEC_OK;
+  if (descs == nullptr || entry_crc == nullptr || (total_chunks > 0 && chunk_crc == nullptr))
+    return PEC_E_INVAL;
+  static const CrcConsts consts = make_consts();
+  cudaStream_t st = as_stream(stream);
+  if (cudaMemsetAsync(entry_crc, 0, sizeof(uint32_t) * (size_t)n, st) != cudaSuccess)
+    return PEC_E_CUDA;
+  if (total_chunks > 0) {
+    const int smem = (kTableWords + kMulWords) * (int)sizeof(uint32_t) + kCrcThreads * kPerThread;
+    if (cudaFuncSetAttribute(pack_crc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess)
+      return PEC_E_CUDA;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_crc_kernel, kCrcThreads, smem);
+    uint64_t grid = (uint64_t)sm_count() * (per_sm < 1 ? 1 : per_sm);
+    if (grid > total_chunks) grid = total_chunks;
+    pack_crc_kernel<<<(unsigned)grid, kCrcThreads, smem, st>>>(descs, n, total_chunks,
+                                                                total_chunks_dev, consts, chunk_crc);
+    uint64_t fold_grid = (total_chunks + 255) / 256;
+    if (fold_grid > (uint64_t)sm_count() * 8) fold_grid = (uint64_t)sm_count() * 8;
+    crc_fold_kernel<<<(unsigned)fold_grid, 256, 0, st>>>(descs, n, total_chunks, total_chunks_dev,
+                                                          consts, chunk_crc, entry_crc);
+  }
+  crc_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(descs, n, consts, entry_crc);
+  return launch_status();
+}
+
+}  // extern "C"

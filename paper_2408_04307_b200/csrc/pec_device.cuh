@@ -1,0 +1,44 @@
+// pec_device.cuh — helpers shared by the PEC kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pec.h"
+
+namespace pecdev {
+
+// SM count of the current device, cached per device id (a pure function of
+// the device, not library state).
+inline int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (cached[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cached[dev] = n;
+  }
+  return cached[dev];
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PEC_OK : PEC_E_CUDA;
+}
+
+// Largest i with first_chunk[i] <= ch (empty descriptors share the next
+// one's first_chunk and are skipped by taking the largest such i).
+__device__ __forceinline__ int find_desc(const pec_copy_desc* __restrict__ d, int n, uint64_t ch) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&d[mid].first_chunk) <= ch) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+}  // namespace pecdev

@@ -19,33 +19,16 @@
 #include <cub/block/block_scan.cuh>
 
 #include "pec.h"
+#include "pec_device.cuh"
 
 namespace {
 
 constexpr int kMaxExperts = 4096;
 
-// ------------------------------------------------------------------------
-// device attribute cache (not state: a pure function of the device id)
-// ------------------------------------------------------------------------
-int sm_count() {
-  static int cached[64] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-  if (dev < 0 || dev >= 64) return 148;
-  if (cached[dev] == 0) {
-    int n = 0;
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-    cached[dev] = n;
-  }
-  return cached[dev];
-}
-
-inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-
-inline int launch_status() {
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? PEC_OK : PEC_E_CUDA;
-}
+using pecdev::as_stream;
+using pecdev::find_desc;
+using pecdev::launch_status;
+using pecdev::sm_count;
 
 // ------------------------------------------------------------------------
 // (a) token histogram
@@ -214,17 +197,6 @@ select_load_aware_kernel(int64_t* __restrict__ counters, int L, int E, int K,
 // ------------------------------------------------------------------------
 // (c)/(d) gather/scatter engines
 // ------------------------------------------------------------------------
-__device__ __forceinline__ int find_desc(const pec_copy_desc* __restrict__ d, int n, uint64_t ch) {
-  // largest i with first_chunk[i] <= ch (empty descriptors share the next
-  // one's first_chunk and are skipped by taking the largest such i)
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(&d[mid].first_chunk) <= ch) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"

@@ -50,21 +50,23 @@ def global_two_tier_select(local_counts, k_snapshot: int, k_persist: int,
 def commit_version(store, version: int, iteration: int, checkpoint_index: int,
                    entries: Sequence[StoreEntry], local_ranks: Iterable[int],
                    payloads: Optional[Mapping[str, object]], group=None,
-                   before_publish: Optional[Callable[[], None]] = None) -> None:
+                   before_publish: Optional[Callable[[], None]] = None,
+                   crcs: Optional[Mapping[str, int]] = None) -> None:
     """Write this process's entries, then publish the version once.
-    ``before_publish`` may raise to abandon the version (no COMPLETE)."""
+    ``before_publish`` may raise to abandon the version (no COMPLETE);
+    ``crcs`` are precomputed entry CRCs (e.g. from pec_pack_crc)."""
     import torch.distributed as dist
     local = set(local_ranks)
     mine = [e for e in entries if e.rank in local]
     world = _world(group)
     if world == 1:
         store.check_version(version)
-        rows = store.write_entries(version, iteration, mine, payloads=payloads)
+        rows = store.write_entries(version, iteration, mine, payloads=payloads, crcs=crcs)
         if before_publish is not None:
             before_publish()
         store.publish(version, iteration, checkpoint_index, entries, rows)
         return
-    rows = store.write_entries(version, iteration, mine, payloads=payloads)
+    rows = store.write_entries(version, iteration, mine, payloads=payloads, crcs=crcs)
     gathered: List[Optional[list]] = [None] * world
     dist.all_gather_object(gathered, rows, group=group)
     err = None

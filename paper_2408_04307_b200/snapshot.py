@@ -72,6 +72,8 @@ class _Inflight:
     pack_done: object = None
     drain_done: object = None
     t_begin: float = 0.0
+    entry_crc: object = None              # pinned int32 [n] (MODE_CRC)
+    crc_keys: object = None
 
 
 class DeviceCheckpointEngine(CheckpointEngine):
@@ -220,6 +222,21 @@ class DeviceCheckpointEngine(CheckpointEngine):
             self._tables[key] = entry
         return entry
 
+    def _launch_pack(self, table: DeviceTable, stream) -> None:
+        """pec_pack, or pec_pack_crc in MODE_CRC (per-entry CRCs land in
+        table.entry_crc on device)."""
+        import torch
+        if self.pack_mode != D.MODE_CRC:
+            D.pack(table.tensor, table.n, table.total_chunks, table.chunk_log2, self.pack_mode,
+                   stream=stream)
+            return
+        if getattr(table, "entry_crc", None) is None:
+            table.chunk_crc = torch.empty(max(1, table.total_chunks), dtype=torch.int32,
+                                          device=self.device)
+            table.entry_crc = torch.empty(max(1, table.n), dtype=torch.int32, device=self.device)
+        D.pack_crc(table.tensor, table.n, table.total_chunks, table.chunk_crc, table.entry_crc,
+                   table.chunk_log2, stream=stream)
+
     # -- snapshot --------------------------------------------------------------------
     def pack_only(self, assignment: PhaseAssignment, plan_key=None, stream=None):
         """Pack the local ranks' ranges into HBM staging without draining
@@ -232,8 +249,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
             s.wait_event(self._staging_free)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(s)
-        D.pack(table.tensor, table.n, table.total_chunks, table.chunk_log2, self.pack_mode,
-               stream=s)
+        self._launch_pack(table, s)
         t1.record(s)
         return t0, t1, sum(l.payload_bytes for l in layouts.values())
 
@@ -258,14 +274,17 @@ class DeviceCheckpointEngine(CheckpointEngine):
         start = torch.cuda.Event(enable_timing=True)
         rec.pack_done = torch.cuda.Event(enable_timing=True)
         start.record(ps)
-        D.pack(table.tensor, table.n, table.total_chunks, table.chunk_log2, self.pack_mode,
-               stream=ps)
+        self._launch_pack(table, ps)
         rec.pack_done.record(ps)
         rec.pack_start = start
         cs.wait_event(rec.pack_done)
         rec.drain_done = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(cs):
             host[:nbytes].copy_(self.staging[:nbytes], non_blocking=True)
+            if self.pack_mode == D.MODE_CRC and table.n:
+                rec.entry_crc = torch.empty(table.n, dtype=torch.int32, pin_memory=True)
+                rec.entry_crc.copy_(table.entry_crc[:table.n], non_blocking=True)
+                rec.crc_keys = [e.store_key for r in self.ranks for e in layouts[r].entries]
         rec.drain_done.record(cs)
         self._staging_free = rec.drain_done
         self._inflight[buf.buffer_id] = rec
@@ -298,8 +317,18 @@ class DeviceCheckpointEngine(CheckpointEngine):
         expanded.record(stream)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        D.pack_indirect(self._dev_table, t.n, t.max_chunks(self.chunk_log2), self._dev_totals,
-                        self.chunk_log2, self.pack_mode, stream=stream)
+        if self.pack_mode == D.MODE_CRC:
+            if getattr(self, "_dev_entry_crc", None) is None:
+                self._dev_chunk_crc = torch.empty(max(1, t.max_chunks(self.chunk_log2)),
+                                                  dtype=torch.int32, device=self.device)
+                self._dev_entry_crc = torch.empty(max(1, t.n), dtype=torch.int32,
+                                                  device=self.device)
+            D.pack_crc(self._dev_table, t.n, t.max_chunks(self.chunk_log2), self._dev_chunk_crc,
+                       self._dev_entry_crc, self.chunk_log2, stream=stream,
+                       totals_dev=self._dev_totals)
+        else:
+            D.pack_indirect(self._dev_table, t.n, t.max_chunks(self.chunk_log2),
+                            self._dev_totals, self.chunk_log2, self.pack_mode, stream=stream)
         t1.record(stream)
         return expanded, t0, t1
 
@@ -360,6 +389,11 @@ class DeviceCheckpointEngine(CheckpointEngine):
         rec.drain_done = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(cs):
             host[:nbytes].copy_(self.staging[:nbytes], non_blocking=True)
+            if self.pack_mode == D.MODE_CRC and self.template.n:
+                # template order; dropped entries carry nbytes 0 (crc 0)
+                rec.entry_crc = torch.empty(self.template.n, dtype=torch.int32, pin_memory=True)
+                rec.entry_crc.copy_(self._dev_entry_crc[:self.template.n], non_blocking=True)
+                rec.crc_keys = [a.store_key for a in self.template.ranges]
         rec.drain_done.record(cs)
         self._staging_free = rec.drain_done
         self._inflight[buf.buffer_id] = rec
@@ -402,6 +436,14 @@ class DeviceCheckpointEngine(CheckpointEngine):
         return {e.store_key: (self.entry_view(buf, e.rank, e.store_key) if e.stop > e.start
                               else memoryview(b"")) for e in entries if e.rank in self.ranks}
 
+    def device_crcs(self, buf: Buffer):
+        """store_key -> CRC-32C computed by the pack (MODE_CRC), else None."""
+        rec = self._inflight.get(buf.buffer_id)
+        if rec is None or rec.entry_crc is None:
+            return None
+        vals = rec.entry_crc.numpy().view(np.uint32)
+        return {k: int(v) for k, v in zip(rec.crc_keys, vals)}
+
     def has_bytes(self, buf: Buffer) -> bool:
         return buf.buffer_id in self._inflight
 
@@ -419,7 +461,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
 
         commit_version(self.store, buf.version, buf.iteration, buf.checkpoint_index, entries,
                        self.ranks, self.payloads(buf, local), group=self.group,
-                       before_publish=abort_check)
+                       before_publish=abort_check, crcs=self.device_crcs(buf))
         return time.perf_counter() - t0
 
     def start_persist(self, buf: Buffer, entries: List[StoreEntry]) -> Future:

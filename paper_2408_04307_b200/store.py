@@ -220,12 +220,17 @@ class DiskStore:
 
     def write_entries(self, version: int, iteration: int, entries: Iterable[StoreEntry],
                       payloads: PayloadSource = None, injector: Optional[TruncatingInjector] = None,
-                      ) -> List[Tuple[str, str, int, int]]:
-        """Entry files of (a subset of) a version; returns manifest rows."""
+                      crcs: Optional[Mapping[str, int]] = None) -> List[Tuple[str, str, int, int]]:
+        """Entry files of (a subset of) a version; returns manifest rows.
+        ``crcs`` supplies precomputed CRC-32Cs (device-computed by the pack);
+        missing ones are computed here."""
         entries = sorted(entries)
         data = self._payloads(entries, version, iteration, payloads)
         vdir = self.version_dir(version)
-        crcs = _crcs(data, self.io_threads if injector is None else 1)
+        if crcs is not None and payloads is not None and all(e.store_key in crcs for e in entries):
+            crcs = [crcs[e.store_key] for e in entries]
+        else:
+            crcs = _crcs(data, self.io_threads if injector is None else 1)
         rows = [(e.store_key, _entry_path(e.rank, e.store_key), _nbytes(p), c)
                 for e, p, c in zip(entries, data, crcs)]
         for r in {e.rank for e in entries}:
@@ -361,7 +366,7 @@ class MemoryStore:
     _pending: Dict[int, Dict[str, bytes]] = field(default_factory=dict)
 
     def write_entries(self, version: int, iteration: int, entries: Iterable[StoreEntry],
-                      payloads: PayloadSource = None, injector=None):
+                      payloads: PayloadSource = None, injector=None, crcs=None):
         if injector is not None:
             raise StoreError("crash injection requires the disk store")
         entries = sorted(entries)

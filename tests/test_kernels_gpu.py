@@ -254,3 +254,40 @@ def test_device_plan_expansion_matches_host_plan(dev, strategy, shape):
             want = O.pack(host_state, copies, tmpl.max_bytes + 512)
             assert np.array_equal(staging.cpu().numpy(), want), (rank, trial)
         del arena
+
+
+@pytest.mark.parametrize("congruent", [True, False])
+def test_pack_crc_copies_and_checksums_every_entry(dev, congruent):
+    """pec_pack_crc: staging bit-exact vs the oracle pack, and each entry's
+    CRC-32C equals the oracle's (C restatement of store.crc32c) over the
+    entry's source bytes — aligned multi-chunk entries, byte-granular and
+    incongruent ranges, partial chunks and empty entries."""
+    import torch
+    from paper_2408_04307_b200 import device as D
+    rng = np.random.default_rng(99 + congruent)
+    size = 24 << 20
+    state = torch.randint(0, 256, (size,), dtype=torch.uint8, device=dev)
+    copies, pos = [], 0
+    lens = [0, 1, 15, 16, 17, 4095, 32768, 32769, 65536, 3 * 32768 + 5, 5 << 20, 100_003]
+    for ln in lens + [int(x) for x in rng.integers(0, 300_000, 20)]:
+        src = int(rng.integers(0, size - ln)) if ln < size else 0
+        if rng.random() < 0.5:
+            src &= ~255  # whole-unit style, 256-aligned
+        dst = pos + ((src - pos) % 256) if congruent else pos + int(rng.integers(0, 64))
+        copies.append((src, dst, ln))
+        pos = dst + ln
+    staging = torch.zeros(pos + 64, dtype=torch.uint8, device=dev)
+    table = np.zeros(len(copies), dtype=D.DESC_DTYPE)
+    for i, (s, t, n) in enumerate(copies):
+        table[i] = (state.data_ptr() + s, staging.data_ptr() + t, n, 0)
+    total = D.plan_chunks(table, 15)
+    dt = torch.from_numpy(table.view(np.uint8).copy()).view(torch.int64).to(dev)
+    chunk = torch.empty(max(1, total), dtype=torch.int32, device=dev)
+    entry = torch.empty(len(copies), dtype=torch.int32, device=dev)
+    D.pack_crc(dt, len(copies), total, chunk, entry)
+    torch.cuda.synchronize()
+    host = state.cpu().numpy()
+    assert np.array_equal(staging.cpu().numpy(), O.pack(host, copies, pos + 64))
+    got = entry.cpu().numpy().view(np.uint32)
+    for (s, _, n), c in zip(copies, got):
+        assert int(c) == O.crc32c(host[s:s + n]), (s, n)

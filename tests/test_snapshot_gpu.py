@@ -225,3 +225,47 @@ def test_fault_mid_snapshot_and_mid_persist_leaves_consistent_state(dev, tmp_pat
     restore(ck.engine, plan)
     assert np.array_equal(arena.buffer.cpu().numpy(), good)
     ck.close()
+
+
+@pytest.mark.parametrize("selection", ["sequential", "load_aware"])
+def test_device_crc_mode_persists_verifiable_versions(dev, tmp_path, selection):
+    """MODE_CRC: the pack computes every entry's CRC-32C; the persist writes
+    them into the manifest without touching the payload on the host, and
+    load_checkpoint's host-side CRC verification accepts every entry."""
+    import torch
+    from paper_2408_04307_b200 import PecConfig, configs
+    from paper_2408_04307_b200 import device as D
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.counting import DeviceTokenCounters
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore, crc32c
+    w = configs.toy()
+    layout = w.layout()
+    L, E = layout.model.num_moe_layers, layout.model.experts_per_layer
+    arena = StateArena(layout, [0], dev, w.expert_tensors)
+    store = DiskStore(tmp_path)
+    counters = None
+    pec = w.pec
+    if selection == "load_aware":
+        counters = DeviceTokenCounters(L, E, dev)
+        pec = PecConfig(k_pec=2, selection="load_aware", k_snapshot=2, k_persist=1)
+    ck = PecCheckpointer(layout, arena, store, pec, w.strategy, i_ckpt=2, counters=counters,
+                         pack_mode=D.MODE_CRC)
+    expected = {}
+    for it in range(1, 9):
+        _mutate(arena, it)
+        ids = torch.randint(0, E, (L, 512), dtype=torch.int32, device=dev)
+        buf = ck.step(it, ids if counters is not None else None)
+        if buf is not None:
+            torch.cuda.synchronize()
+            expected[buf.version] = _expected_entries(arena.buffer.cpu().numpy(), arena,
+                                                      buf.content, [0])
+            ck.wait_pack()
+    ck.finish()
+    assert store.complete_versions() == sorted(expected)
+    for v in store.complete_versions():
+        data = store.load_checkpoint(v)   # verifies every manifest CRC on the host
+        for k, b in data.items():
+            assert b == expected[v][k]
+            assert store.manifest(v).entries[k][2] == crc32c(b)
+    ck.close()
