@@ -1,0 +1,14 @@
+"""Import shim: `mocsim` -> paper_2408_04307_b200 (test infrastructure only).
+
+Lets the reference's OWN test files for the in-scope modules run unchanged
+against this package (tests/test_reference_suite.py), as a drop-in check.
+"""
+import sys
+
+import paper_2408_04307_b200 as _pkg
+from paper_2408_04307_b200 import *  # noqa: F401,F403
+from paper_2408_04307_b200 import engine, planner, selector, store, topology  # noqa: F401
+
+for _name in ("engine", "planner", "selector", "store", "topology"):
+    sys.modules[f"mocsim.{_name}"] = getattr(_pkg, _name)
+__version__ = _pkg.__version__

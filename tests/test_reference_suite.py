@@ -1,0 +1,36 @@
+"""Drop-in check: the reference's own unit tests for the in-scope modules
+(topology, planner, selector, engine, store) run unchanged against this
+package through a `mocsim` import shim (tests/compat/mocsim).
+
+Reads /root/reference in place (never copied); skipped where the reference
+is not mounted (e.g. on the GPU box)."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+REF_TESTS = Path("/root/reference/pkg/tests")
+ROOT = Path(__file__).resolve().parent.parent
+FILES = ["test_topology.py", "test_planner.py", "test_selector.py", "test_engine.py",
+         "test_store.py"]
+
+
+@pytest.mark.skipif(not REF_TESTS.exists(), reason="reference not mounted")
+def test_reference_unit_tests_pass_against_this_package(tmp_path):
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([str(ROOT / "tests" / "compat"), str(REF_TESTS),
+                                         str(ROOT)])
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+           "--rootdir", str(tmp_path), *[str(REF_TESTS / f) for f in FILES]]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, cwd=tmp_path, timeout=600)
+    tail = "\n".join(res.stdout.splitlines()[-15:])
+    assert res.returncode == 0, tail
+    assert " passed" in tail and "failed" not in tail, tail
+    # the shim really routed to this package
+    probe = subprocess.run([sys.executable, "-c", "import mocsim; print(mocsim.__file__)"],
+                           env=env, capture_output=True, text=True, cwd=tmp_path)
+    assert "tests/compat/mocsim" in probe.stdout
