@@ -269,3 +269,47 @@ def test_device_crc_mode_persists_verifiable_versions(dev, tmp_path, selection):
             assert b == expected[v][k]
             assert store.manifest(v).entries[k][2] == crc32c(b)
     ck.close()
+
+
+def test_empty_shards_and_ragged_ranges_round_trip(dev, tmp_path):
+    """Edge shapes the reference admits: an other-states blob smaller than
+    dp (last shard is empty: ceil split 3 over 4 -> 1,1,1,0), an expert weight
+    of odd size split across 2 EP groups, and a 1-parameter module."""
+    import torch
+    from paper_2408_04307_b200 import PecConfig
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.restore import restore
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore
+    layout = make_layout(n_experts=2, dp=4, ep=2, gpus_per_node=2, n_layers=1, epp=7,
+                         b_w=1, b_o=4, p_ne=1001, other=3,
+                         modules=(("a", 1000), ("b", 1)))
+    assert layout.by_key["other.r3"].size_bytes == 0
+    arena = StateArena(layout, range(4), dev)
+    store = DiskStore(tmp_path)
+    ck = PecCheckpointer(layout, arena, store, PecConfig(k_pec=1), "equal_pec", i_ckpt=1,
+                         async_persist=False)
+    snaps = {}
+    for it in (1, 2):
+        _mutate(arena, it)
+        buf = ck.step(it)
+        torch.cuda.synchronize()
+        snaps[buf.version] = arena.buffer.cpu().numpy().copy()
+        ck.wait_pack()
+    ck.finish()
+    for v in store.complete_versions():
+        data = store.load_checkpoint(v)
+        assert data["other.r3"] == b""
+        parts = sorted(k for k in data if k.startswith("ew."))
+        assert len(parts) == 2 and [len(data[k]) for k in parts] == [3, 4]  # floor split of 7
+    plan = ck.engine.resolve_recovery({0})
+    ck.engine.on_fault({0})
+    arena.buffer.zero_()
+    restore(ck.engine, plan)
+    now = arena.buffer.cpu().numpy()
+    for key, d in plan.decisions.items():
+        if arena.has(key) and d.source != "initial":
+            s = arena.slot(key)
+            assert np.array_equal(now[s.offset:s.offset + s.size],
+                                  snaps[d.version][s.offset:s.offset + s.size]), key
+    ck.close()
