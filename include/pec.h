@@ -141,7 +141,7 @@ int pec_pack_indirect(const pec_copy_desc* descs, int n, uint64_t max_chunks,
  * Same copy as pec_pack (vectorised engine) and, in the same pass over the
  * bytes, entry_crc[i] = CRC-32C of descriptor i's nbytes (== pec_crc32c of
  * the staged entry).  chunk_log2 must be 15; chunk_crc is device scratch of
- * total_chunks uint32; entry_crc is device memory of n uint32.
+ * 8 * total_chunks uint32 (one per 4 KiB); entry_crc is device memory of n uint32.
  * total_chunks_dev (nullable) caps the chunk count from device memory, as in
  * pec_pack_indirect (device-expanded plans). */
 int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,

@@ -105,16 +105,21 @@ __device__ __forceinline__ uint32_t mul_const(const uint32_t* nib, uint32_t b) {
   return r;
 }
 
+// Work unit = one warp x 4 KiB (8 units per 32 KiB chunk).  Warps take
+// units independently (no block barrier on the hot path): unit u of the
+// launch is warp-global index + k * total_warps, so neighbouring warps stream
+// neighbouring 4 KiB and every warp keeps its own loads in flight.
+constexpr int kUnitLog2 = 12;
+constexpr int kUnitsPerChunk = 1 << (kCrcLg - kUnitLog2);
+
 __global__ void __launch_bounds__(kCrcThreads, 2)
 pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
                 const uint64_t* __restrict__ total_dev, CrcConsts k,
-                uint32_t* __restrict__ chunk_raw) {
+                uint32_t* __restrict__ unit_raw) {
   // dynamic smem: byte table | nibble tables | per-warp 4 KiB transpose tiles
   extern __shared__ __align__(16) uint32_t table[];
   uint32_t* nib = table + kTableWords;
   uint32_t* stage = table + kTableWords + kMulWords;
-  __shared__ uint32_t warp_raw[kCrcThreads / 32];
-  __shared__ uint32_t warp_len[kCrcThreads / 32];
   if (total_dev != nullptr) {
     const uint64_t td = *total_dev;
     total = td < total ? td : total;
@@ -134,14 +139,24 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
   const uint32_t* tab = table + lane;
   const uint32_t* s32 = nib;                 // x^(8*32)
   const uint32_t* lvl = nib + 128;           // lane tree levels, 128 words each
-  const uint32_t* wlv = nib + 6 * 128;       // warp tree levels
+  int4* tile = reinterpret_cast<int4*>(stage) + warp * 256;
 
-  for (uint64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
-    const int i = find_desc(d, n, ch);
-    const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << kCrcLg;
+  const uint64_t units = total * kUnitsPerChunk;
+  const uint64_t warps_total = (uint64_t)gridDim.x * (kCrcThreads / 32);
+  pecdev::DescCursor cur;
+  for (uint64_t u = (uint64_t)blockIdx.x * (kCrcThreads / 32) + warp; u < units;
+       u += warps_total) {
+    const uint64_t ch = u >> (kCrcLg - kUnitLog2);
+    const int i = cur.find(d, n, ch);
     const uint64_t nb = __ldg(&d[i].nbytes);
-    const uint64_t span = 1ull << kCrcLg;
+    const uint64_t off = ((ch - __ldg(&d[i].first_chunk)) << kCrcLg) +
+                         ((u & (kUnitsPerChunk - 1)) << kUnitLog2);
+    const uint64_t span = 1ull << kUnitLog2;
     const uint64_t len = off >= nb ? 0 : (nb - off < span ? nb - off : span);
+    if (len == 0) {
+      if (lane == 0) unit_raw[u] = 0u;
+      continue;
+    }
     const uint8_t* s = reinterpret_cast<const uint8_t*>(__ldg(&d[i].src) + off);
     uint8_t* t = reinterpret_cast<uint8_t*>(__ldg(&d[i].dst) + off);
     const bool fast = len == span && ((reinterpret_cast<uintptr_t>(s) |
@@ -149,51 +164,46 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
     uint32_t c = 0;
     uint32_t my_len;
     if (fast) {
-      // Coalesced: lane l of warp w moves 16-byte units l + 32k of the warp's
-      // 4 KiB (global -> registers -> staging), and parks them in a swizzled
-      // per-warp shared tile; then each lane reads back ITS contiguous 128 B
-      // (units 8l..8l+7) conflict-free and folds them as four independent
-      // 32-byte CRC chains.  Swizzle: unit u lives at 16-byte slot
-      // u ^ ((u >> 3) & 7), so both access patterns hit 8 distinct 16-byte
-      // bank groups per 8 lanes.
-      const int4* vs = reinterpret_cast<const int4*>(s) + warp * 256;
-      int4* vt = reinterpret_cast<int4*>(t) + warp * 256;
-      int4* tile = reinterpret_cast<int4*>(stage) + warp * 256;
+      // coalesced 16 B units (lane + 32k) -> staging, and into a swizzled tile
+      // from which each lane reads back ITS contiguous 128 B conflict-free
+      // (16-byte slot of unit x: x ^ ((x >> 3) & 7)); four 32-byte CRC chains.
+      const int4* vs = reinterpret_cast<const int4*>(s);
+      int4* vt = reinterpret_cast<int4*>(t);
       int4 r[kVecPerThread];
 #pragma unroll
-      for (int u = 0; u < kVecPerThread; ++u) r[u] = __ldg(vs + lane + 32 * u);
+      for (int q = 0; q < kVecPerThread; ++q) r[q] = __ldg(vs + lane + 32 * q);
 #pragma unroll
-      for (int u = 0; u < kVecPerThread; ++u) {
-        __stcs(vt + lane + 32 * u, r[u]);
-        const int unit = lane + 32 * u;
-        tile[unit ^ ((unit >> 3) & 7)] = r[u];
+      for (int q = 0; q < kVecPerThread; ++q) {
+        __stcs(vt + lane + 32 * q, r[q]);
+        const int x = lane + 32 * q;
+        tile[x ^ ((x >> 3) & 7)] = r[q];
       }
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < kVecPerThread; ++j) {
-        const int unit = lane * kVecPerThread + j;
-        r[j] = tile[unit ^ ((unit >> 3) & 7)];
+        const int x = lane * kVecPerThread + j;
+        r[j] = tile[x ^ ((x >> 3) & 7)];
       }
-      uint32_t q[4] = {0u, 0u, 0u, 0u};
+      uint32_t q4[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int h = 0; h < 2; ++h) {
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
 #pragma unroll
-          for (int ch4 = 0; ch4 < 4; ++ch4) {
-            const int4 v = r[ch4 * 2 + u];
+          for (int cc = 0; cc < 4; ++cc) {
+            const int4 v = r[cc * 2 + h];
             const uint32_t word = w == 0 ? (uint32_t)v.x : w == 1 ? (uint32_t)v.y
                                 : w == 2 ? (uint32_t)v.z : (uint32_t)v.w;
-            q[ch4] = fold_word(tab, q[ch4], word);
+            q4[cc] = fold_word(tab, q4[cc], word);
           }
         }
       }
-      __syncwarp();  // the tile is rewritten by the next chunk
-      c = mul_const(s32, mul_const(s32, mul_const(s32, q[0]) ^ q[1]) ^ q[2]) ^ q[3];
+      __syncwarp();  // the tile is rewritten by this warp's next unit
+      c = mul_const(s32, mul_const(s32, mul_const(s32, q4[0]) ^ q4[1]) ^ q4[2]) ^ q4[3];
       my_len = kPerThread;
     } else {
-      // general chunk (unaligned head, partial tail): bytes, still 128 per thread
-      const uint64_t lo = (uint64_t)tid * kPerThread;
+      // partial or unaligned unit: bytes, 128 per lane
+      const uint64_t lo = (uint64_t)lane * kPerThread;
       const uint64_t hi = lo + kPerThread < len ? lo + kPerThread : len;
       for (uint64_t b = lo; b < hi; ++b) {
         const uint8_t v = s[b];
@@ -202,7 +212,7 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
       }
       my_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
     }
-    // warp tree: lanes hold consecutive pieces; fold right neighbours in
+    // warp tree: lanes hold consecutive 128 B pieces; fold right neighbours in
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
       const uint32_t oc = __shfl_down_sync(0xffffffffu, c, 1 << j);
@@ -212,41 +222,25 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
         my_len += ol;
       }
     }
-    if (lane == 0) {
-      warp_raw[warp] = c;
-      warp_len[warp] = my_len;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      // cross-warp tree over the 8 warp registers (lanes 0..7)
-      uint32_t a = lane < kCrcThreads / 32 ? warp_raw[lane] : 0u;
-      uint32_t al = lane < kCrcThreads / 32 ? warp_len[lane] : 0u;
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const uint32_t oc = __shfl_down_sync(0xffffffffu, a, 1 << j);
-        const uint32_t ol = __shfl_down_sync(0xffffffffu, al, 1 << j);
-        if ((lane & ((2 << j) - 1)) == 0) {
-          a = (fast ? mul_const(wlv + j * 128, a) : shift_bytes(k.x2k, a, ol)) ^ oc;
-          al += ol;
-        }
-      }
-      if (lane == 0) chunk_raw[ch] = a;
-    }
-    __syncthreads();
+    if (lane == 0) unit_raw[u] = c;
   }
 }
 
+// One thread per chunk: join the chunk's 8 unit registers (constant 4 KiB
+// shifts for full units), shift by the bytes that follow the chunk in its
+// entry and XOR into the entry register.
 __global__ void crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
                                 const uint64_t* __restrict__ total_dev, CrcConsts k,
-                                const uint32_t* __restrict__ chunk_raw,
+                                const uint32_t* __restrict__ unit_raw,
                                 uint32_t* __restrict__ entry_raw) {
+  __shared__ uint32_t x2k[64];
+  if (threadIdx.x < 64) x2k[threadIdx.x] = k.x2k[threadIdx.x];
+  __syncthreads();
   if (total_dev != nullptr) {
     const uint64_t td = *total_dev;
     total = td < total ? td : total;
   }
-  __shared__ uint32_t x2k[64];
-  if (threadIdx.x < 64) x2k[threadIdx.x] = k.x2k[threadIdx.x];
-  __syncthreads();
+  const uint32_t unit_shift = k.mul[6];  // x^(8 * 4096)
   for (uint64_t ch = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < total;
        ch += (uint64_t)gridDim.x * blockDim.x) {
     const int i = find_desc(d, n, ch);
@@ -254,7 +248,15 @@ __global__ void crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint
     const uint64_t nb = __ldg(&d[i].nbytes);
     if (off >= nb) continue;
     const uint64_t end = off + (1ull << kCrcLg) < nb ? off + (1ull << kCrcLg) : nb;
-    atomicXor(&entry_raw[i], shift_bytes(x2k, chunk_raw[ch], nb - end));
+    uint32_t acc = unit_raw[ch * kUnitsPerChunk];
+    for (int w = 1; w < kUnitsPerChunk; ++w) {
+      const uint64_t uoff = off + ((uint64_t)w << kUnitLog2);
+      if (uoff >= end) break;
+      const uint64_t ulen = end - uoff < (1ull << kUnitLog2) ? end - uoff : (1ull << kUnitLog2);
+      acc = (ulen == (1ull << kUnitLog2) ? gf2_mul(unit_shift, acc) : shift_bytes(x2k, acc, ulen))
+            ^ unit_raw[ch * kUnitsPerChunk + w];
+    }
+    atomicXor(&entry_raw[i], shift_bytes(x2k, acc, nb - end));
   }
 }
 
@@ -305,14 +307,15 @@ int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
   if (cudaMemsetAsync(entry_crc, 0, sizeof(uint32_t) * (size_t)n, st) != cudaSuccess)
     return PEC_E_CUDA;
   if (total_chunks > 0) {
-    const int smem = (kTableWords + kMulWords) * (int)sizeof(uint32_t) + kCrcThreads * kPerThread;
+    const int smem = (kTableWords + kMulWords) * (int)sizeof(uint32_t) + kCrcThreads * 128;
     if (cudaFuncSetAttribute(pack_crc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem) != cudaSuccess)
       return PEC_E_CUDA;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_crc_kernel, kCrcThreads, smem);
     uint64_t grid = (uint64_t)sm_count() * (per_sm < 1 ? 1 : per_sm);
-    if (grid > total_chunks) grid = total_chunks;
+    const uint64_t need = (total_chunks * kUnitsPerChunk + kCrcThreads / 32 - 1) / (kCrcThreads / 32);
+    if (grid > need) grid = need;
     pack_crc_kernel<<<(unsigned)grid, kCrcThreads, smem, st>>>(descs, n, total_chunks,
                                                                 total_chunks_dev, consts, chunk_crc);
     uint64_t fold_grid = (total_chunks + 255) / 256;

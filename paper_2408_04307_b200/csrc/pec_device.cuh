@@ -41,4 +41,28 @@ __device__ __forceinline__ int find_desc(const pec_copy_desc* __restrict__ d, in
   return lo;
 }
 
+// Monotone cursor over the table for a CTA walking chunk indices upward
+// (ch = blockIdx.x, + gridDim.x, ...): resumes from the previous descriptor
+// instead of a fresh binary search, so the common case is one L1-resident
+// load of the next descriptor's first_chunk rather than a chain of
+// dependent global loads per chunk.
+struct DescCursor {
+  int i = -1;
+  __device__ __forceinline__ int find(const pec_copy_desc* __restrict__ d, int n, uint64_t ch) {
+    if (i < 0 || __ldg(&d[i].first_chunk) > ch) {
+      i = find_desc(d, n, ch);
+      return i;
+    }
+    int steps = 0;
+    while (i + 1 < n && __ldg(&d[i + 1].first_chunk) <= ch) {
+      if (++steps > 8) {  // far jump: binary search instead
+        i = find_desc(d, n, ch);
+        return i;
+      }
+      ++i;
+    }
+    return i;
+  }
+};
+
 }  // namespace pecdev

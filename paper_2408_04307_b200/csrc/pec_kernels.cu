@@ -264,8 +264,9 @@ copy_vec_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
     const uint64_t t = *total_dev;  // written by pec_expand_plan earlier on the stream
     total = t < total ? t : total;
   }
+  pecdev::DescCursor cur;
   for (uint64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
-    const int i = find_desc(d, n, ch);
+    const int i = cur.find(d, n, ch);
     const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << lg;
     const uint64_t nb = __ldg(&d[i].nbytes);
     if (off >= nb) continue;  // empty descriptor (never for a well-formed table)
@@ -335,9 +336,9 @@ struct ChunkView {
 };
 
 __device__ __forceinline__ ChunkView chunk_view(const pec_copy_desc* __restrict__ d, int n,
-                                                uint64_t ch, int lg) {
+                                                uint64_t ch, int lg, pecdev::DescCursor& cur) {
   ChunkView v;
-  const int i = find_desc(d, n, ch);
+  const int i = cur.find(d, n, ch);
   const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << lg;
   const uint64_t nb = __ldg(&d[i].nbytes);
   const uint64_t span = 1ull << lg;
@@ -370,10 +371,11 @@ struct Piece {
 };
 
 __device__ __forceinline__ Piece piece_of(const pec_copy_desc* __restrict__ d, int n, int lg,
-                                          uint64_t j, uint32_t per_chunk, int piece_log2) {
+                                          uint64_t j, uint32_t per_chunk, int piece_log2,
+                                          pecdev::DescCursor& cur) {
   const uint64_t jc = j / per_chunk;
   const uint32_t jp = (uint32_t)(j % per_chunk);
-  const ChunkView v = chunk_view(d, n, blockIdx.x + jc * gridDim.x, lg);
+  const ChunkView v = chunk_view(d, n, blockIdx.x + jc * gridDim.x, lg, cur);
   Piece p;
   const uint64_t lo = (uint64_t)jp << piece_log2;
   const uint64_t hi = lo + (1ull << piece_log2);
@@ -409,8 +411,9 @@ copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
     const uint64_t items = chunks * per_chunk;
     uint32_t bytes_of[kBulkStages];
     uint8_t* dst_of[kBulkStages];
+    pecdev::DescCursor cur;  // items are issued in increasing chunk order
     auto issue = [&](uint64_t j, int s) {
-      const Piece p = piece_of(d, n, lg, j, per_chunk, piece_log2);
+      const Piece p = piece_of(d, n, lg, j, per_chunk, piece_log2, cur);
       bytes_of[s] = p.bytes;
       dst_of[s] = p.dst;
       if (p.bytes) {
@@ -438,8 +441,9 @@ copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
     // ---- edge workers: unaligned heads/tails and incongruent chunks -----
     const int wid = threadIdx.x - 32;  // warps 1..3 (96 threads)
     if (wid >= 0) {
+      pecdev::DescCursor cur;
       for (uint64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
-        const ChunkView v = chunk_view(d, n, ch, lg);
+        const ChunkView v = chunk_view(d, n, ch, lg, cur);
         if (v.body == 0 && v.len > 0) {
           // incongruent or tiny chunk: plain copy by the 96 edge threads
           const uintptr_t sa = reinterpret_cast<uintptr_t>(v.s);

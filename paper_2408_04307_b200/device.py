@@ -33,6 +33,7 @@ TEMPLATE_DTYPE = np.dtype([("src_offset", "<u8"), ("nbytes", "<u8"), ("layer", "
 DEFAULT_CHUNK_LOG2 = 15  # 32 KiB work chunks
 
 MODE_AUTO, MODE_VEC, MODE_BULK = 0, 1, 2
+CRC_UNITS_PER_CHUNK = 8  # pec_pack_crc scratch: one uint32 per 4 KiB of every 32 KiB chunk
 MODE_CRC = 3  # engine-level: vectorised pack with fused per-entry CRC-32C (pec_pack_crc)
 
 _lib = None
@@ -236,11 +237,12 @@ def expand_plan(tmpl_dev, n: int, sel, state_base: int, stage_base: int, out_dev
 def pack_crc(desc_dev, n: int, total_chunks: int, chunk_crc_dev, entry_crc_dev,
              chunk_log2: int = DEFAULT_CHUNK_LOG2, stream=None, totals_dev=None) -> None:
     """pec_pack with the CRC-32C of every entry computed in the same pass
-    (entry_crc_dev [n] int32/uint32 device; chunk_crc_dev [total] scratch)."""
+    (entry_crc_dev [n] int32 device; chunk_crc_dev [8 * total] scratch)."""
     import torch
     if n == 0:
         return
-    if chunk_crc_dev.numel() < max(1, total_chunks) or entry_crc_dev.numel() < n:
+    if chunk_crc_dev.numel() < max(1, CRC_UNITS_PER_CHUNK * total_chunks) \
+            or entry_crc_dev.numel() < n:
         raise SpecValidationError("crc buffers large enough", "chunk/entry crc buffers too small")
     tdev = _dev_ptr(totals_dev, torch.int64, "totals") if totals_dev is not None else None
     rc = lib().pec_pack_crc(_dev_ptr(desc_dev, desc_dev.dtype, "descriptor table"), n,

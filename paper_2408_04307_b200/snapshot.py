@@ -231,8 +231,8 @@ class DeviceCheckpointEngine(CheckpointEngine):
                    stream=stream)
             return
         if getattr(table, "entry_crc", None) is None:
-            table.chunk_crc = torch.empty(max(1, table.total_chunks), dtype=torch.int32,
-                                          device=self.device)
+            table.chunk_crc = torch.empty(max(1, D.CRC_UNITS_PER_CHUNK * table.total_chunks),
+                                          dtype=torch.int32, device=self.device)
             table.entry_crc = torch.empty(max(1, table.n), dtype=torch.int32, device=self.device)
         D.pack_crc(table.tensor, table.n, table.total_chunks, table.chunk_crc, table.entry_crc,
                    table.chunk_log2, stream=stream)
@@ -319,8 +319,9 @@ class DeviceCheckpointEngine(CheckpointEngine):
         t0.record(stream)
         if self.pack_mode == D.MODE_CRC:
             if getattr(self, "_dev_entry_crc", None) is None:
-                self._dev_chunk_crc = torch.empty(max(1, t.max_chunks(self.chunk_log2)),
-                                                  dtype=torch.int32, device=self.device)
+                self._dev_chunk_crc = torch.empty(
+                    max(1, D.CRC_UNITS_PER_CHUNK * t.max_chunks(self.chunk_log2)),
+                    dtype=torch.int32, device=self.device)
                 self._dev_entry_crc = torch.empty(max(1, t.n), dtype=torch.int32,
                                                   device=self.device)
             D.pack_crc(self._dev_table, t.n, t.max_chunks(self.chunk_log2), self._dev_chunk_crc,

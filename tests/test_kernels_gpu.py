@@ -282,7 +282,7 @@ def test_pack_crc_copies_and_checksums_every_entry(dev, congruent):
         table[i] = (state.data_ptr() + s, staging.data_ptr() + t, n, 0)
     total = D.plan_chunks(table, 15)
     dt = torch.from_numpy(table.view(np.uint8).copy()).view(torch.int64).to(dev)
-    chunk = torch.empty(max(1, total), dtype=torch.int32, device=dev)
+    chunk = torch.empty(max(1, D.CRC_UNITS_PER_CHUNK * total), dtype=torch.int32, device=dev)
     entry = torch.empty(len(copies), dtype=torch.int32, device=dev)
     D.pack_crc(dt, len(copies), total, chunk, entry)
     torch.cuda.synchronize()
