@@ -288,7 +288,6 @@ copy_vec_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
 // tail, and any chunk whose src/dst are not congruent mod 16, are copied by
 // the other warps with plain loads/stores in parallel.
 constexpr int kBulkThreads = 128;
-constexpr int kBulkStages = 6;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -319,6 +318,18 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
 __device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                :: "l"(gmem), "r"(smem_u32(smem)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* smem, const void* gmem, uint32_t bytes,
+                                              uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;"
+      :: "r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* gmem, const void* smem, uint32_t bytes,
+                                              uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+               :: "l"(gmem), "r"(smem_u32(smem)), "r"(bytes), "l"(policy) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
@@ -362,7 +373,6 @@ __device__ __forceinline__ ChunkView chunk_view(const pec_copy_desc* __restrict_
 // Pipeline items are pieces of <= kStageBytes of a chunk's aligned body:
 // item j of this CTA is piece (j % P) of its (j / P)-th chunk, P = pieces per
 // chunk, so chunk sizes above one stage simply yield more items.
-constexpr int kStageLog2 = 15;
 
 struct Piece {
   const uint8_t* src;
@@ -386,9 +396,12 @@ __device__ __forceinline__ Piece piece_of(const pec_copy_desc* __restrict__ d, i
   return p;
 }
 
-__global__ void __launch_bounds__(kBulkThreads, 1)
+template <int kStages, int kSLog2, bool kHint>
+__global__ void __launch_bounds__(kBulkThreads)
 copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
                  const uint64_t* __restrict__ total_dev, int lg) {
+  constexpr int kBulkStages = kStages;
+  constexpr int kStageLog2 = kSLog2;
   extern __shared__ __align__(128) uint8_t ring[];  // kBulkStages * stage
   if (total_dev != nullptr) {
     const uint64_t t = *total_dev;
@@ -412,13 +425,18 @@ copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
     uint32_t bytes_of[kBulkStages];
     uint8_t* dst_of[kBulkStages];
     pecdev::DescCursor cur;  // items are issued in increasing chunk order
+    uint64_t policy = 0;
+    if (kHint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     auto issue = [&](uint64_t j, int s) {
       const Piece p = piece_of(d, n, lg, j, per_chunk, piece_log2, cur);
       bytes_of[s] = p.bytes;
       dst_of[s] = p.dst;
       if (p.bytes) {
         mbar_expect_tx(&bars[s], p.bytes);
-        bulk_g2s(ring + (uint64_t)s * stage_bytes, p.src, p.bytes, &bars[s]);
+        if (kHint)
+          bulk_g2s_hint(ring + (uint64_t)s * stage_bytes, p.src, p.bytes, &bars[s], policy);
+        else
+          bulk_g2s(ring + (uint64_t)s * stage_bytes, p.src, p.bytes, &bars[s]);
       } else {
         mbar_arrive(&bars[s]);  // keep the stage's phase sequence in step
       }
@@ -428,7 +446,12 @@ copy_bulk_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
     for (uint64_t j = 0; j < items; ++j) {
       const int s = (int)(j % kBulkStages);
       mbar_wait(&bars[s], (uint32_t)((j / kBulkStages) & 1u));
-      if (bytes_of[s]) bulk_s2g(dst_of[s], ring + (uint64_t)s * stage_bytes, bytes_of[s]);
+      if (bytes_of[s]) {
+        if (kHint)
+          bulk_s2g_hint(dst_of[s], ring + (uint64_t)s * stage_bytes, bytes_of[s], policy);
+        else
+          bulk_s2g(dst_of[s], ring + (uint64_t)s * stage_bytes, bytes_of[s]);
+      }
       bulk_commit();  // one group per item (possibly empty) keeps counts exact
       // refill the stage consumed one step earlier with item j-1+kStages
       if (j >= 1 && j - 1 + kBulkStages < items) {
@@ -572,58 +595,82 @@ expand_plan_kernel(const pec_plan_template* __restrict__ tmpl, int n,
   }
 }
 
-// Per-device launch geometry, computed once (attribute setting and
-// occupancy queries are host round trips that would otherwise sit between
-// the caller's start event and the kernel).
-struct CopyGeometry {
+// Per-device launch geometry, computed once per kernel variant (attribute
+// setting and occupancy queries are host round trips that would otherwise
+// sit between the caller's start event and the kernel).
+struct Geometry {
   int ready = 0;
-  int vec_grid = 0;
-  int bulk_grid = 0;
-  int bulk_smem = 0;
+  int grid = 0;
+  int smem = 0;
 };
 
-int copy_geometry(CopyGeometry** out) {
-  static CopyGeometry geo[64];
+template <int kStages, int kSLog2, bool kHint, int kMaxPerSM = 64>
+int launch_bulk(const pec_copy_desc* descs, int n, uint64_t total, const uint64_t* total_dev,
+                int lg, cudaStream_t st) {
+  static Geometry geo[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return PEC_E_CUDA;
-  CopyGeometry& g = geo[dev];
+  Geometry& g = geo[dev];
+  auto kern = copy_bulk_kernel<kStages, kSLog2, kHint>;
   if (!g.ready) {
-    const int sms = sm_count();
-    g.bulk_smem = kBulkStages << kStageLog2;
-    if (cudaFuncSetAttribute(copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             g.bulk_smem) != cudaSuccess)
+    g.smem = kStages << kSLog2;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem) !=
+        cudaSuccess)
       return PEC_E_CUDA;
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_bulk_kernel, kBulkThreads, g.bulk_smem);
-    g.bulk_grid = sms * (per_sm < 1 ? 1 : per_sm);
-    per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_vec_kernel, kVecThreads, 0);
-    g.vec_grid = sms * (per_sm < 1 ? 1 : per_sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBulkThreads, g.smem);
+    if (per_sm > kMaxPerSM) per_sm = kMaxPerSM;
+    g.grid = sm_count() * (per_sm < 1 ? 1 : per_sm);
     g.ready = 1;
   }
-  *out = &g;
-  return PEC_OK;
+  const int smem = kStages << (lg < kSLog2 ? lg : kSLog2);
+  const uint64_t grid = (uint64_t)g.grid < total ? (uint64_t)g.grid : total;
+  kern<<<(unsigned)grid, kBulkThreads, smem, st>>>(descs, n, total, total_dev, lg);
+  return launch_status();
 }
 
+int launch_vec(const pec_copy_desc* descs, int n, uint64_t total, const uint64_t* total_dev,
+               int lg, cudaStream_t st) {
+  static Geometry geo[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return PEC_E_CUDA;
+  Geometry& g = geo[dev];
+  if (!g.ready) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_vec_kernel, kVecThreads, 0);
+    g.grid = sm_count() * (per_sm < 1 ? 1 : per_sm);
+    g.ready = 1;
+  }
+  const uint64_t grid = (uint64_t)g.grid < total ? (uint64_t)g.grid : total;
+  copy_vec_kernel<<<(unsigned)grid, kVecThreads, 0, st>>>(descs, n, total, total_dev, lg);
+  return launch_status();
+}
+
+// mode 1: vector engine; 2: TMA bulk engine (the default); 10-16: bulk-engine
+// ring/occupancy variants kept for benchmarking (tools/pack_variants.py).
 int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, const uint64_t* total_dev,
                 int lg, int mode, void* stream) {
   if (n < 0 || lg < 12 || lg > 24) return PEC_E_INVAL;
-  if (mode < 0 || mode > 2) return PEC_E_INVAL;
+  const bool known = (mode >= 0 && mode <= 2) || (mode >= 10 && mode <= 16);
+  if (!known) return PEC_E_INVAL;
   if (total == 0 || n == 0) return PEC_OK;
   if (descs == nullptr) return PEC_E_INVAL;
-  CopyGeometry* g = nullptr;
-  const int rc = copy_geometry(&g);
-  if (rc != PEC_OK) return rc;
   cudaStream_t st = as_stream(stream);
-  if (mode == 2) {
-    const int smem = kBulkStages << (lg < kStageLog2 ? lg : kStageLog2);
-    const uint64_t grid = (uint64_t)g->bulk_grid < total ? (uint64_t)g->bulk_grid : total;
-    copy_bulk_kernel<<<(unsigned)grid, kBulkThreads, smem, st>>>(descs, n, total, total_dev, lg);
-    return launch_status();
+  switch (mode) {
+    case 1: return launch_vec(descs, n, total, total_dev, lg, st);
+    case 10: return launch_bulk<3, 15, false, 1>(descs, n, total, total_dev, lg, st);
+    case 11: return launch_bulk<2, 15, false, 1>(descs, n, total, total_dev, lg, st);
+    case 12: return launch_bulk<4, 15, false, 1>(descs, n, total, total_dev, lg, st);
+    case 13: return launch_bulk<4, 14, false, 1>(descs, n, total, total_dev, lg, st);
+    case 14: return launch_bulk<3, 15, true, 1>(descs, n, total, total_dev, lg, st);
+    case 15: return launch_bulk<2, 16, false, 1>(descs, n, total, total_dev, lg, st);
+    case 16: return launch_bulk<6, 15, false, 1>(descs, n, total, total_dev, lg, st);
+    // default (measured best on B200, tools/pack_variants.py): one CTA per
+    // SM, 3 x 32 KiB stages (two loads in flight while one stage drains),
+    // L2 evict_first on both directions (streamed once; keeps L2 for the
+    // training kernels the pack overlaps with)
+    default: return launch_bulk<3, 15, true, 1>(descs, n, total, total_dev, lg, st);
   }
-  const uint64_t grid = (uint64_t)g->vec_grid < total ? (uint64_t)g->vec_grid : total;
-  copy_vec_kernel<<<(unsigned)grid, kVecThreads, 0, st>>>(descs, n, total, total_dev, lg);
-  return launch_status();
 }
 
 }  // namespace
