@@ -360,7 +360,7 @@ def run_b200(args):
                          counters=counters, control_group=control, pack_mode=mode,
                          chunk_log2=args.chunk_log2)
     eng = ck.engine
-    eng._ensure_staging(ck.max_snapshot_bytes())
+    eng.reserve(ck.max_snapshot_bytes(), host_buffers=0)
     k_s = w.pec.k_snapshot
     sel = torch.empty((L, min(k_s, E)), dtype=torch.int32, device=dev)
     stream = eng.pack_stream
@@ -446,8 +446,7 @@ def run_b200(args):
         # pins ~2 GB/s; a training job does this at start-up): 3 with a
         # persist tier, 2 without (buffers then recycle through RECOVERY)
         tpin = time.perf_counter()
-        for b in range(3 if store is not None else 2):
-            eng._ensure_host(b, eng.staging.numel())
+        eng.reserve(eng.staging.numel(), host_buffers=3 if store is not None else 2)
         pin_s = time.perf_counter() - tpin
     link_alone = link_conc = None
     if not args.no_e2e:
@@ -503,11 +502,10 @@ def run_b200(args):
             h2d += ids_host[k].numel() * 4
             counters.add_iteration(ids_dev)
             buf = ck.checkpoint(it)               # select + plan + pack + drain
-            ck._complete(buf)                     # wait for SNAPSHOTTED
-            rec = eng._inflight[buf.buffer_id]
-            first = rec.layouts[rank].entries[0]
+            ck.wait_snapshot(buf)                 # wait for SNAPSHOTTED
+            first = eng.snapshot_layout(buf, rank).entries[0]
             _ = int(eng.entry_view(buf, rank, first.store_key)[0])  # host read
-            d2h += rec.nbytes
+            d2h += eng.snapshot_nbytes(buf)
         e2e_s = time.perf_counter() - tw
         e2e_s = max_over_ranks(e2e_s, world, dev)
         e2e_moved = sum_over_ranks(sum(eng.stats["snap_bytes"][-e2e_steps:]), world, dev)
@@ -538,10 +536,10 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
         if plan is not None:
-            first_layout = eng._table_for(plan.assignments[0], ("phase", 0))[1][rank]
+            first_layout = eng.layouts_for(plan.assignments[0], ("phase", 0))[rank]
         else:
-            first_layout = eng._inflight[max(eng._inflight)].layouts[rank] if eng._inflight \
-                else StagingLayout.build(pt.ranges, arena, rank)
+            first_layout = StagingLayout.build(pt.select({m: frozenset({m % E})
+                                                          for m in range(L)}), arena, rank)
         gbs, desc = cpu_pack_sample(first_layout.entries, int(args.cpu_sample_gb * 1e9), threads,
                                     args.cpu_seconds)
         cpu = {"value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",

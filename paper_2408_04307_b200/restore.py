@@ -108,11 +108,11 @@ def _pieces(engine, plan: RecoveryPlan, wanted, slot_bytes: int):
                         if b.version == d.version and b.snapshot_completed), None)
             if buf is None or not engine.has_bytes(buf):
                 raise RuntimeError(f"memory source v{d.version} for {key} is not in this process")
-            rec = engine._inflight[buf.buffer_id]
             found = False
             for r in layout.ranks_of_node(d.node):  # only the decided (surviving) node
-                if r in rec.layouts:                 # this process's pinned buffer: H2D
-                    st, base0, kind = rec.layouts[r], rec.region[r], "host"
+                if r in engine.ranks:                # this process's pinned buffer: H2D
+                    st, base0, kind = (engine.snapshot_layout(buf, r),
+                                       engine.snapshot_region(buf, r), "host")
                     src = engine.host[buf.buffer_id]
                 else:                                # a peer process's node-shared buffer
                     peer = peers.get((r, d.version))

@@ -195,12 +195,30 @@ class DeviceCheckpointEngine(CheckpointEngine):
             return shb, st
         return None
 
-    def reserve(self, nbytes: int) -> None:
-        """Pre-allocate staging and all host buffers (pinning is slow: do it
-        once, before training)."""
+    def reserve(self, nbytes: int, host_buffers: Optional[int] = None) -> None:
+        """Pre-allocate the staging buffer and (the first ``host_buffers``
+        of) the pinned host buffers (pinning is slow: do it once, before
+        training)."""
         self._ensure_staging(nbytes)
-        for i in range(len(self.host)):
+        n = len(self.host) if host_buffers is None else min(host_buffers, len(self.host))
+        for i in range(n):
             self._ensure_host(i, nbytes)
+
+    def layouts_for(self, assignment: PhaseAssignment, plan_key=None) -> Dict[int, StagingLayout]:
+        """Staging layout of every local rank for an assignment (cached per
+        plan key)."""
+        return self._table_for(assignment, plan_key)[1]
+
+    def snapshot_layout(self, buf: Buffer, rank: int) -> StagingLayout:
+        """Staging / host-buffer layout of ``rank``'s entries in ``buf``."""
+        return self._inflight[buf.buffer_id].layouts[rank]
+
+    def snapshot_region(self, buf: Buffer, rank: int) -> int:
+        """Byte offset of ``rank``'s region in ``buf``'s host buffer."""
+        return self._inflight[buf.buffer_id].region[rank]
+
+    def snapshot_nbytes(self, buf: Buffer) -> int:
+        return self._inflight[buf.buffer_id].nbytes
 
     # -- plan -> device table ------------------------------------------------------
     def _table_for(self, assignment: PhaseAssignment, key=None):
@@ -672,6 +690,11 @@ class PecCheckpointer:
 
     def wait_pack(self, stream=None) -> None:
         self.engine.wait_pack(stream=stream)
+
+    def wait_snapshot(self, buf: Buffer) -> None:
+        """Block until ``buf``'s drain landed (SNAPSHOTTED) and start its
+        persist when it is next in line."""
+        self._complete(buf)
 
     def _complete(self, buf: Buffer) -> None:
         promoted = self.engine.complete_snapshot(buf)

@@ -209,7 +209,7 @@ def test_fault_mid_snapshot_and_mid_persist_leaves_consistent_state(dev, tmp_pat
     assert b1.status == FREE
     ck.hold_persist(True)
     b2 = ck.step(2)
-    ck._complete(b2)                   # SNAPSHOTTED -> PERSISTING, held (not started)
+    ck.wait_snapshot(b2)               # SNAPSHOTTED -> PERSISTING, held (not started)
     ck.hold_persist(False)             # persist starts in the background ...
     ck.engine.on_fault(set())          # ... and is aborted before publishing (or won)
     assert store.complete_versions() in ([], [b2.version])

@@ -136,12 +136,13 @@ def main():
             b.synchronize()
             times.append(a.elapsed_time(b))
         ok = True
-        table, layouts, region, nbytes = eng._table_for(ph, ("k", k))
+        layouts = eng.layouts_for(ph, ("k", k))
+        base = 0
         for r, st in layouts.items():
-            base = region[r]
             for e in st.entries:
                 ok &= bool(torch.equal(eng.staging[base + e.stage_offset:base + e.stage_offset + e.nbytes],
                                        arena.buffer[e.src_offset:e.src_offset + e.nbytes]))
+            base += (st.nbytes + 255) // 256 * 256
         total = sum(st.payload_bytes for st in layouts.values())
         sweep.append({"k": k, "period": plan_k.period, "bytes_all_ranks": total,
                       "planner_total": sum(plan_k.workload_bytes[0].values()),
