@@ -60,7 +60,7 @@ def arena_slots(layout: RankLayout, ranks: Sequence[int]) -> Dict[str, UnitSlot]
     slots: Dict[str, UnitSlot] = {}
     off = 0
     for u in layout.units:
-        if u.size_bytes == 0 or not (u.replica_ranks & rs):
+        if u.size_bytes <= 0 or not (u.replica_ranks & rs):
             continue
         slots[u.key] = UnitSlot(u.key, u.kind, off, u.size_bytes)
         off = _align(off + u.size_bytes)

@@ -1,0 +1,73 @@
+"""Host-side staging layout and device-plan template properties (CPU)."""
+
+import json
+import random
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from paper_2408_04307_b200 import ClusterSpec, ModelSpec, ParallelSpec, build_layout
+from paper_2408_04307_b200 import build_phase_assignment
+from paper_2408_04307_b200.arena import PeerSlots, arena_slots
+from paper_2408_04307_b200.staging import STAGE_ALIGN, PlanTemplate, StagingLayout
+
+SMALL = json.loads((GOLDEN / "plans.json").read_text())["small"]
+
+
+def _layout(case):
+    m = case["model"]
+    model = ModelSpec(**{**m, "non_expert_modules": tuple(map(tuple, m["non_expert_modules"]))})
+    gpn = case["gpus_per_node"]
+    return build_layout(model, ParallelSpec(case["dp"], case["ep"]),
+                        ClusterSpec(num_nodes=case["dp"] // gpn, gpus_per_node=gpn))
+
+
+@pytest.mark.parametrize("i", range(0, len(SMALL), 3))
+def test_staging_layout_invariants(i):
+    layout = _layout(SMALL[i])
+    due = {int(m): frozenset(v) for m, v in SMALL[i]["due"].items()}
+    for strat in ("baseline", "equal_pec", "adaptive_pec"):
+        phase = build_phase_assignment(layout, due, strat)
+        for r, ranges in phase.items():
+            slots = PeerSlots(layout, r)
+            st = StagingLayout.build(ranges, slots, r)
+            prev_end = 0
+            for e in st.entries:
+                assert e.stage_offset >= prev_end                          # ordered, no overlap
+                assert e.stage_offset - prev_end < STAGE_ALIGN             # bounded padding
+                assert (e.stage_offset - e.src_offset) % STAGE_ALIGN == 0  # congruent source
+                prev_end = e.stage_offset + e.nbytes
+            assert st.nbytes == prev_end
+            # (the reference admits negative "other" shards when other_states_bytes
+            # is tiny vs dp: ceil split 5 over 4 -> 2,2,2,-1; they carry no bytes)
+            assert st.payload_bytes == sum(max(0, a.stop - a.start) for a in ranges)
+            table, total = st.descriptors(1 << 40, 1 << 41, chunk_log2=12)
+            assert int(table["nbytes"].sum()) == st.payload_bytes
+            assert total == sum(-(-int(n) // 4096) for n in table["nbytes"])
+
+
+@pytest.mark.parametrize("i", range(len(SMALL)))
+def test_plan_template_selects_exactly_the_planner_ranges(i):
+    """The device-plan template filtered by any due set equals the reference
+    planner's ranges for that rank (equal/baseline placement)."""
+    layout = _layout(SMALL[i])
+    rng = random.Random(i)
+    n = layout.model.experts_per_layer
+    for strat in ("equal_pec", "baseline"):
+        for r in range(layout.n_ranks):
+            tmpl = PlanTemplate(layout, PeerSlots(layout, r), r, strat, "cpu")
+            for _ in range(4):
+                due = {m: frozenset(rng.sample(range(n), rng.randint(0, n)))
+                       for m in range(layout.model.num_moe_layers)}
+                want = tuple(a for a in build_phase_assignment(layout, due, strat).get(r, ())
+                             if a.stop > a.start)
+                assert tmpl.select(due) == want
+
+
+def test_arena_slots_cover_exactly_the_resident_units():
+    layout = _layout(SMALL[5])
+    for r in range(layout.n_ranks):
+        got = set(arena_slots(layout, [r]))
+        want = {u.key for u in layout.units if r in u.replica_ranks and u.size_bytes}
+        assert got == want
