@@ -169,6 +169,20 @@ def _pieces(engine, plan: RecoveryPlan, wanted, slot_bytes: int):
 _READ_STEP = 4 << 20  # CRC each 4 MiB right after reading it, while cache-hot
 
 
+def _read_piece_raw(item) -> None:
+    """Read a file piece into the pinned slot (CRC verified on the GPU)."""
+    p, off, host = item
+    view = memoryview(host.numpy()).cast("B")[off:off + p.nbytes]
+    with open(p.path, "rb", buffering=0) as f:
+        f.seek(p.file_off)
+        got = 0
+        while got < p.nbytes:
+            n = f.readinto(view[got:])
+            if not n:
+                raise ChecksumMismatchError(p.entry, "short read")
+            got += n
+
+
 def _read_piece(item) -> int:
     p, off, host = item
     view = memoryview(host.numpy()).cast("B")[off:off + p.nbytes]
@@ -186,12 +200,28 @@ def _read_piece(item) -> int:
     return crc
 
 
+def _chain(running: Dict[str, int], p: "_Piece", crc: int) -> None:
+    """Fold a piece's CRC into its entry's running CRC; verify at the end."""
+    prev = running.get(p.entry)
+    running[p.entry] = crc if prev is None else D.crc32c_combine(prev, crc, p.nbytes)
+    if p.last and running.pop(p.entry) != p.entry_crc:
+        raise ChecksumMismatchError(p.entry, "crc32c mismatch")
+
+
 def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
             chunk_log2: int = D.DEFAULT_CHUNK_LOG2, stream=None,
-            slot_bytes: int = 256 << 20, io_threads: int = 16) -> RestoreReport:
+            slot_bytes: int = 256 << 20, io_threads: int = 16,
+            verify: str = "device") -> RestoreReport:
     """Execute ``plan`` for the units resident in ``engine.arena`` (or the
     given subset ``keys``).  ``engine`` is a DeviceCheckpointEngine whose
-    ``store`` (a DiskStore) holds the storage versions."""
+    ``store`` (a DiskStore) holds the storage versions.
+
+    ``verify="device"`` checks every storage entry's CRC-32C on the GPU: the
+    scatter runs as `pec_pack_crc`, which checksums each piece while moving
+    it, and the host only chains the per-piece CRCs; ``"host"`` checksums
+    while reading the files.  A mismatch raises ChecksumMismatchError."""
+    if verify not in ("device", "host"):
+        raise ValueError("verify must be 'device' or 'host'")
     import time
     import torch
     t_start = time.perf_counter()
@@ -228,6 +258,12 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
     s.wait_stream(torch.cuda.current_stream(dev))  # e.g. initial fills / prior wipes
     running: Dict[str, int] = {}   # entry -> chained CRC of the pieces read so far
     timers = []
+    checks = []                    # (batch, pinned per-piece CRCs) for device verification
+    max_pieces = max(len(b) for b in batches)
+    crc_scratch = [None, None]
+    crc_host = torch.empty(len(pieces) if verify == "device" else 1, dtype=torch.int32,
+                           pin_memory=True)
+    crc_pos = 0
     with ThreadPoolExecutor(max_workers=io_threads) as pool:
         for bi, batch in enumerate(batches):
             slot = bi % 2
@@ -235,7 +271,11 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
                 ring.free[slot].synchronize()   # slot's previous batch fully consumed
             hslot, dslot = ring.host[slot], ring.dev[slot]
             files = [(p, off, hslot) for p, off in batch if p.kind == "file"]
-            crcs = list(pool.map(_read_piece, files))
+            if verify == "device":
+                list(pool.map(_read_piece_raw, files))
+                crcs = None
+            else:
+                crcs = list(pool.map(_read_piece, files))
             for p, off in batch:
                 if p.kind == "bytes":
                     hslot.numpy()[off:off + p.nbytes] = np.frombuffer(
@@ -245,11 +285,9 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
                     else:
                         rep.storage_bytes += p.nbytes
             files_or_bytes = [(p, off) for p, off in batch if p.kind in ("file", "bytes")]
-            for (p, _, _), c in zip(files, crcs):
-                prev = running.get(p.entry)
-                running[p.entry] = c if prev is None else D.crc32c_combine(prev, c, p.nbytes)
-                if p.last and running.pop(p.entry) != p.entry_crc:
-                    raise ChecksumMismatchError(p.entry, "crc32c mismatch")
+            for i_f, (p, _, _) in enumerate(files):
+                if crcs is not None:
+                    _chain(running, p, crcs[i_f])
                 rep.storage_bytes += p.nbytes
             table = np.zeros(len(batch), dtype=D.DESC_DTYPE)
             with torch.cuda.stream(s):
@@ -268,12 +306,33 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
             dt = DeviceTable(table, nchunks, dev, chunk_log2)
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0.record(s)
-            D.unpack(dt.tensor, dt.n, dt.total_chunks, chunk_log2, engine.pack_mode, stream=s)
+            if verify == "device" and files:
+                # per-slot scratch (reused only after the slot's event), one pinned
+                # CRC array for the whole restore (no pinning inside the loop)
+                need = max(1, D.CRC_UNITS_PER_CHUNK * nchunks)
+                if crc_scratch[slot] is None or crc_scratch[slot][0].numel() < need:
+                    crc_scratch[slot] = (torch.empty(need, dtype=torch.int32, device=dev),
+                                         torch.empty(max(1, max_pieces), dtype=torch.int32,
+                                                     device=dev))
+                scratch, ecrc = crc_scratch[slot]
+                D.pack_crc(dt.tensor, dt.n, dt.total_chunks, scratch, ecrc, chunk_log2, stream=s)
+                hcrc = crc_host[crc_pos:crc_pos + dt.n]
+                crc_pos += dt.n
+                with torch.cuda.stream(s):
+                    hcrc.copy_(ecrc[:dt.n], non_blocking=True)
+                checks.append((batch, hcrc))
+            else:
+                D.unpack(dt.tensor, dt.n, dt.total_chunks, chunk_log2, D.MODE_AUTO, stream=s)
             t1.record(s)
             timers.append((t0, t1, dt))
             ring.free[slot] = t1
     torch.cuda.current_stream(dev).wait_stream(s)
     s.synchronize()
+    for batch, hcrc in checks:            # batches in order: pieces chain in file order
+        vals = hcrc.numpy().view(np.uint32)
+        for i, (p, _) in enumerate(batch):
+            if p.kind == "file":
+                _chain(running, p, int(vals[i]))
     for peer in peers.values():
         if peer is not None:
             peer[0].close()
