@@ -94,7 +94,9 @@ class DeviceCheckpointEngine(CheckpointEngine):
         self.pack_mode = pack_mode
         self.chunk_log2 = chunk_log2
         self.group = control_group
-        self.pack_stream = torch.cuda.Stream(device=self.device)
+        # high priority: when the pack and training kernels both have CTAs
+        # waiting, the pack (the only training-blocking part) goes first
+        self.pack_stream = torch.cuda.Stream(device=self.device, priority=-1)
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self.staging = None
         self.host: List[Optional[object]] = [None] * n_buffers
