@@ -236,13 +236,16 @@ def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float):
 
     run(False, 0)  # warm
     without = run(False, 0)
+    n_before = len(ck.engine.stats["pack_ms"])
     with_ = run(True, 10 ** 6)
     ck.finish()
+    packs = ck.engine.stats["pack_ms"][n_before:]
     return {"i_ckpt": i_ckpt, "iters": iters, "checkpoints": iters // i_ckpt,
             "fb_ms": round(n_gemm * gemm_ms, 1), "fb_gemms": n_gemm,
             "update_ms": round(update_ms, 2),
             "iter_ms_without": round(without, 3), "iter_ms_with": round(with_, 3),
             "exposed_ms_per_iter": round(with_ - without, 3),
+            "pack_ms_in_loop": round(statistics.mean(packs), 3) if packs else None,
             "overhead_frac": round((with_ - without) / without, 5)}
 
 
