@@ -32,6 +32,7 @@ extern "C" {
 #define PEC_E_INVAL (-1)   /* bad argument (maps to SpecValidationError / ValueError) */
 #define PEC_E_CUDA (-2)    /* CUDA launch or runtime error (maps to RuntimeError)   */
 #define PEC_E_RANGE (-3)   /* size exceeds a kernel limit (e.g. experts > 4096)     */
+#define PEC_E_IO (-4)      /* file I/O failed (maps to OSError)                      */
 
 #define PEC_ABI_VERSION 1
 
@@ -165,6 +166,16 @@ uint32_t pec_crc32c_combine(uint32_t crc_a, uint32_t crc_b, uint64_t len_b);
  * to `threads` host threads (large regions are split and combined). */
 int pec_crc32c_many(const void* base, const uint64_t* offs,
                     const uint64_t* lens, int n, uint32_t* out, int threads);
+
+/* ---- native persist writer -------------------- *
+ * Replaces: the entry-file loop of DiskStore.write_version (store.py:210-216).
+ * Writes file i = lens[i] bytes from host buffer bufs[i] with a pool of up to
+ * `threads` threads (pwrite of <= 16 MiB pieces, large files in parallel);
+ * with crc_out != NULL also returns each file's CRC-32C, computed per piece
+ * right after writing it.  flags bit 0: fsync each file.  PEC_E_IO on any
+ * open/write/fsync/close failure. */
+int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
+                    int n, uint32_t* crc_out, int threads, int flags);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -688,6 +688,7 @@ const char* pec_strerror(int code) {
     case PEC_E_INVAL: return "invalid argument";
     case PEC_E_CUDA: return "CUDA launch/runtime error";
     case PEC_E_RANGE: return "size exceeds a kernel limit";
+    case PEC_E_IO: return "file I/O failed";
     default: return "unknown error";
   }
 }

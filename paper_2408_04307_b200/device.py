@@ -23,6 +23,7 @@ PEC_OK = 0
 PEC_E_INVAL = -1
 PEC_E_CUDA = -2
 PEC_E_RANGE = -3
+PEC_E_IO = -4
 
 # numpy mirror of `pec_copy_desc`
 DESC_DTYPE = np.dtype([("src", "<u8"), ("dst", "<u8"), ("nbytes", "<u8"),
@@ -70,6 +71,7 @@ def _load():
         "pec_crc32c": (c_u32, [vp, ctypes.c_size_t, c_u32]),
         "pec_crc32c_combine": (c_u32, [c_u32, c_u32, c_u64]),
         "pec_crc32c_many": (c_int, [vp, vp, vp, c_int, vp, c_int]),
+        "pec_write_files": (c_int, [vp, vp, vp, c_int, vp, c_int, c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -91,7 +93,7 @@ def exported_symbols():
     return ["pec_abi_version", "pec_strerror", "pec_token_hist", "pec_select_sequential",
             "pec_select_load_aware", "pec_pack", "pec_unpack", "pec_plan_chunks",
             "pec_expand_plan", "pec_pack_indirect", "pec_pack_crc",
-            "pec_crc32c", "pec_crc32c_combine", "pec_crc32c_many"]
+            "pec_crc32c", "pec_crc32c_combine", "pec_crc32c_many", "pec_write_files"]
 
 
 def _check(rc: int, what: str) -> None:
@@ -100,6 +102,8 @@ def _check(rc: int, what: str) -> None:
     text = lib().pec_strerror(rc).decode()
     if rc in (PEC_E_INVAL, PEC_E_RANGE):
         raise SpecValidationError(f"{what} arguments", text)
+    if rc == PEC_E_IO:
+        raise OSError(f"{what}: {text}")
     raise PecKernelError(f"{what}: {text} (code {rc})")
 
 
@@ -316,5 +320,28 @@ def crc32c_many(base, offsets, lengths, threads: Optional[int] = None) -> np.nda
     rc = lib().pec_crc32c_many(addr, offs.ctypes.data, lens.ctypes.data, len(offs),
                                out.ctypes.data, int(threads))
     _check(rc, "pec_crc32c_many")
+    del keep
+    return out
+
+
+def write_files(paths, buffers, threads: Optional[int] = None, want_crc: bool = True,
+                fsync: bool = False):
+    """Native multi-threaded writer (pec_write_files): file i <- buffers[i]
+    (bytes-like / ndarray / CPU tensor).  Returns the CRC-32C of each file
+    (uint32 ndarray) when ``want_crc``."""
+    n = len(paths)
+    keep = [_host_buffer(b) for b in buffers]
+    c_paths = (ctypes.c_char_p * n)(*[os.fsencode(str(p)) for p in paths])
+    c_bufs = (ctypes.c_void_p * n)(*[k[0] for k in keep])
+    lens = np.array([k[1] for k in keep], dtype=np.uint64)
+    out = np.zeros(n, dtype=np.uint32) if want_crc else None
+    if threads is None:
+        threads = max(1, len(os.sched_getaffinity(0)))
+    rc = lib().pec_write_files(ctypes.cast(c_paths, ctypes.c_void_p),
+                               ctypes.cast(c_bufs, ctypes.c_void_p),
+                               lens.ctypes.data if n else None, n,
+                               out.ctypes.data if want_crc and n else None, int(threads),
+                               1 if fsync else 0)
+    _check(rc, "pec_write_files")
     del keep
     return out

@@ -227,14 +227,22 @@ class DiskStore:
         entries = sorted(entries)
         data = self._payloads(entries, version, iteration, payloads)
         vdir = self.version_dir(version)
-        if crcs is not None and payloads is not None and all(e.store_key in crcs for e in entries):
-            crcs = [crcs[e.store_key] for e in entries]
-        else:
-            crcs = _crcs(data, self.io_threads if injector is None else 1)
-        rows = [(e.store_key, _entry_path(e.rank, e.store_key), _nbytes(p), c)
-                for e, p, c in zip(entries, data, crcs)]
         for r in {e.rank for e in entries}:
             (vdir / f"rank{r:04d}").mkdir(parents=True, exist_ok=True)
+        given = crcs is not None and payloads is not None and \
+            all(e.store_key in crcs for e in entries)
+        if injector is None and payloads is not None and entries:
+            # native writer: threads pwrite <= 16 MiB pieces (large entries in
+            # parallel) and CRC each piece right after writing it
+            paths = [vdir / _entry_path(e.rank, e.store_key) for e in entries]
+            got = _dev.write_files(paths, data, threads=self.io_threads, want_crc=not given)
+            crc_list = [crcs[e.store_key] for e in entries] if given else [int(c) for c in got]
+            return [(e.store_key, _entry_path(e.rank, e.store_key), _nbytes(p), c)
+                    for e, p, c in zip(entries, data, crc_list)]
+        crc_list = [crcs[e.store_key] for e in entries] if given else \
+            _crcs(data, self.io_threads if injector is None else 1)
+        rows = [(e.store_key, _entry_path(e.rank, e.store_key), _nbytes(p), c)
+                for e, p, c in zip(entries, data, crc_list)]
         if injector is not None or self.io_threads == 1 or len(entries) < 2:
             for (_, rel, _, _), p in zip(rows, data):
                 self._put(vdir / rel, p, injector)
