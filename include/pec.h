@@ -170,7 +170,7 @@ int pec_crc32c_many(const void* base, const uint64_t* offs,
 /* ---- native persist writer -------------------- *
  * Replaces: the entry-file loop of DiskStore.write_version (store.py:210-216).
  * Writes file i = lens[i] bytes from host buffer bufs[i] with a pool of up to
- * `threads` threads (pwrite of <= 16 MiB pieces, large files in parallel);
+ * `threads` threads (whole files per thread, largest first, 4 MiB writes);
  * with crc_out != NULL also returns each file's CRC-32C, computed per piece
  * right after writing it.  flags bit 0: fsync each file.  PEC_E_IO on any
  * open/write/fsync/close failure. */

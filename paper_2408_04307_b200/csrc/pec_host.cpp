@@ -235,12 +235,12 @@ int pec_crc32c_many(const void* base, const uint64_t* offs, const uint64_t* lens
   return PEC_OK;
 }
 
-// Native persist writer: file i receives lens[i] bytes from bufs[i].  Files
-// are cut into <= 16 MiB pieces that a pool of threads writes with pwrite (a
-// multi-GB entry is written by several threads at once); unless crc_out is
-// NULL each piece is checksummed right after it is written, while it is
-// still cache-hot, and the pieces' CRCs are combined per file — one pass
-// over the payload instead of a CRC pass plus a write pass.
+// Native persist writer: file i receives lens[i] bytes from bufs[i].  A pool
+// of threads takes whole files, largest first (tmpfs/ext4 serialise writers
+// of one inode, so files, not byte ranges, are the unit of parallelism), and
+// writes each sequentially in 4 MiB pieces; unless crc_out is NULL each piece
+// is checksummed right after it is written, while it is still cache-hot, so
+// the payload is read once for both.
 // flags bit 0: fsync every file before returning.
 int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
                     int n, uint32_t* crc_out, int threads, int flags) {
@@ -248,64 +248,53 @@ int pec_write_files(const char* const* paths, const void* const* bufs, const uin
     return PEC_E_INVAL;
   if (n == 0) return PEC_OK;
   if (threads < 1) threads = 1;
-  std::vector<int> fds(n, -1);
-  int rc = PEC_OK;
-  for (int i = 0; i < n; ++i) {
-    fds[i] = open(paths[i], O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
-    if (fds[i] < 0) { rc = PEC_E_IO; break; }
-  }
-  constexpr uint64_t kPiece = 16ull << 20;
-  struct Piece { int file; uint64_t off, len; uint32_t crc; };
-  std::vector<Piece> pieces;
-  std::vector<size_t> first(n + 1, 0);
-  if (rc == PEC_OK) {
-    for (int i = 0; i < n; ++i) {
-      first[i] = pieces.size();
-      for (uint64_t o = 0; o < lens[i]; o += kPiece)
-        pieces.push_back(Piece{i, o, std::min<uint64_t>(kPiece, lens[i] - o), 0});
-    }
-    first[n] = pieces.size();
-    std::atomic<size_t> next{0};
-    std::atomic<int> failed{0};
-    auto work = [&]() {
-      for (size_t k = next.fetch_add(1); k < pieces.size(); k = next.fetch_add(1)) {
-        if (failed.load()) return;
-        Piece& p = pieces[k];
-        const uint8_t* src = static_cast<const uint8_t*>(bufs[p.file]) + p.off;
+  constexpr uint64_t kPiece = 4ull << 20;
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return lens[a] > lens[b]; });
+  std::atomic<int> next{0};
+  std::atomic<int> failed{0};
+  auto work = [&]() {
+    for (int k = next.fetch_add(1); k < n; k = next.fetch_add(1)) {
+      if (failed.load()) return;
+      const int i = order[k];
+      const int fd = open(paths[i], O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
+      if (fd < 0) {
+        failed.store(1);
+        return;
+      }
+      const uint8_t* src = static_cast<const uint8_t*>(bufs[i]);
+      uint32_t crc = 0;
+      bool ok = true;
+      for (uint64_t off = 0; off < lens[i] && ok; off += kPiece) {
+        const uint64_t len = std::min<uint64_t>(kPiece, lens[i] - off);
         uint64_t done = 0;
-        while (done < p.len) {
-          const ssize_t w = pwrite(fds[p.file], src + done, p.len - done, (off_t)(p.off + done));
+        while (done < len) {
+          const ssize_t w = write(fd, src + off + done, len - done);
           if (w < 0) {
             if (errno == EINTR) continue;
-            failed.store(1);
-            return;
+            ok = false;
+            break;
           }
           done += (uint64_t)w;
         }
-        if (crc_out != nullptr) p.crc = crc_impl(src, p.len, 0);
+        if (ok && crc_out != nullptr) crc = crc_impl(src + off, len, crc);
       }
-    };
-    const int nt = (int)std::min<size_t>((size_t)threads, std::max<size_t>(pieces.size(), 1));
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
-    work();
-    for (auto& th : pool) th.join();
-    if (failed.load()) rc = PEC_E_IO;
-  }
-  for (int i = 0; i < n; ++i) {
-    if (fds[i] < 0) continue;
-    if (rc == PEC_OK && (flags & 1) && fsync(fds[i]) != 0) rc = PEC_E_IO;
-    if (close(fds[i]) != 0 && rc == PEC_OK) rc = PEC_E_IO;
-  }
-  if (rc == PEC_OK && crc_out != nullptr) {
-    for (int i = 0; i < n; ++i) {
-      uint32_t c = 0;
-      for (size_t k = first[i]; k < first[i + 1]; ++k)
-        c = combine_impl(c, pieces[k].crc, pieces[k].len);
-      crc_out[i] = c;
+      if (ok && (flags & 1) && fsync(fd) != 0) ok = false;
+      if (close(fd) != 0) ok = false;
+      if (!ok) {
+        failed.store(1);
+        return;
+      }
+      if (crc_out != nullptr) crc_out[i] = crc;
     }
-  }
-  return rc;
+  };
+  const int nt = std::min(threads, n);
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  return failed.load() ? PEC_E_IO : PEC_OK;
 }
 
 }  // extern "C"

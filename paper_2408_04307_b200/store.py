@@ -232,8 +232,8 @@ class DiskStore:
         given = crcs is not None and payloads is not None and \
             all(e.store_key in crcs for e in entries)
         if injector is None and payloads is not None and entries:
-            # native writer: threads pwrite <= 16 MiB pieces (large entries in
-            # parallel) and CRC each piece right after writing it
+            # native writer: threads take whole files (largest first) and CRC
+            # each 4 MiB piece right after writing it
             paths = [vdir / _entry_path(e.rank, e.store_key) for e in entries]
             got = _dev.write_files(paths, data, threads=self.io_threads, want_crc=not given)
             crc_list = [crcs[e.store_key] for e in entries] if given else [int(c) for c in got]
