@@ -101,3 +101,17 @@ def test_oracle_pack_unpack_roundtrip():
     back = O.unpack(st, copies, np.zeros_like(state))
     for s, _, n in copies:
         assert np.array_equal(back[s:s + n], state[s:s + n])
+
+
+def test_native_writer_writes_exact_bytes_and_crcs(tmp_path):
+    from paper_2408_04307_b200 import device as D
+    from paper_2408_04307_b200.store import crc32c
+    rng = np.random.default_rng(8)
+    bufs = [rng.integers(0, 256, size=n, dtype=np.uint8) for n in (0, 1, 4097, (4 << 20) + 5)]
+    paths = [tmp_path / f"e{i}.bin" for i in range(len(bufs))]
+    crcs = D.write_files(paths, bufs, threads=3)
+    for p, b, c in zip(paths, bufs, crcs):
+        assert p.read_bytes() == b.tobytes()
+        assert int(c) == crc32c(b)
+    with pytest.raises(OSError):
+        D.write_files([tmp_path / "missing" / "x.bin"], [bufs[2]])
