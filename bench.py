@@ -449,8 +449,17 @@ def run_b200(args):
         # pins ~2 GB/s; a training job does this at start-up): 3 with a
         # persist tier, 2 without (buffers then recycle through RECOVERY)
         tpin = time.perf_counter()
-        eng.reserve(eng.staging.numel(), host_buffers=3 if store is not None else 2)
+        pin_error = None
+        try:
+            eng.reserve(eng.staging.numel(), host_buffers=3 if store is not None else 2)
+        except (RuntimeError, MemoryError) as exc:  # e.g. host RAM too small to pin
+            pin_error = f"{type(exc).__name__}: {exc}"[:200]
         pin_s = time.perf_counter() - tpin
+        if max_over_ranks(1.0 if pin_error else 0.0, world, dev) > 0:
+            # every rank skips the host-buffer legs together (no stranded collectives)
+            print(f"bench: pinned host buffers unavailable ({pin_error}); "
+                  "skipping e2e and stall legs", file=sys.stderr)
+            args.no_e2e = args.no_stall = True
     link_alone = link_conc = None
     if not args.no_e2e:
         # host-link roofline measured in this run (1 GiB pinned D2H, best of 3,
