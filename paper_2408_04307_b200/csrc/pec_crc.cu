@@ -307,13 +307,18 @@ int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
   if (cudaMemsetAsync(entry_crc, 0, sizeof(uint32_t) * (size_t)n, st) != cudaSuccess)
     return PEC_E_CUDA;
   if (total_chunks > 0) {
-    const int smem = (kTableWords + kMulWords) * (int)sizeof(uint32_t) + kCrcThreads * 128;
-    if (cudaFuncSetAttribute(pack_crc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem) != cudaSuccess)
-      return PEC_E_CUDA;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_crc_kernel, kCrcThreads, smem);
-    uint64_t grid = (uint64_t)sm_count() * (per_sm < 1 ? 1 : per_sm);
+    // launch geometry once per process (attribute/occupancy queries are not free)
+    static const int smem = (kTableWords + kMulWords) * (int)sizeof(uint32_t) + kCrcThreads * 128;
+    static const int per_sm = [] {
+      if (cudaFuncSetAttribute(pack_crc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem) != cudaSuccess)
+        return 0;
+      int blocks = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pack_crc_kernel, kCrcThreads, smem);
+      return blocks < 1 ? 1 : blocks;
+    }();
+    if (per_sm == 0) return PEC_E_CUDA;
+    uint64_t grid = (uint64_t)sm_count() * per_sm;
     const uint64_t need = (total_chunks * kUnitsPerChunk + kCrcThreads / 32 - 1) / (kCrcThreads / 32);
     if (grid > need) grid = need;
     pack_crc_kernel<<<(unsigned)grid, kCrcThreads, smem, st>>>(descs, n, total_chunks,
