@@ -181,6 +181,44 @@ def cpu_pack_sample(entries, sample_bytes: int, threads: int, min_seconds: float
     return payload * reps / dt / 1e9, desc
 
 
+def cpu_components(layout, strategy: str, k_pec: int, crc_sample: int = 1 << 20):
+    """The reference's other per-checkpoint CPU costs:
+    two-tier load-aware selection (oracle restatement of the reference's
+    Python sort, selector.py:91-100 / simulator.py:339-354), one checkpoint's
+    range plan (build_phase_assignment, planner.py:263-295) and the
+    reference's byte-at-a-time pure-Python CRC-32C (store.py:49-70,
+    restated in the oracle) on a 1 MiB sample, 1 core."""
+    from oracle import pec_oracle as O
+    from paper_2408_04307_b200 import build_phase_assignment
+    m = layout.model
+    L, E = m.num_moe_layers, m.experts_per_layer
+    rng = np.random.default_rng(1)
+    snap = rng.integers(0, 1 << 20, (L, E))
+    pers = snap.copy()
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < 0.5:
+        O.two_tier_load_aware(snap.copy(), pers.copy(), k_pec, k_pec)
+        reps += 1
+    sel_us = (time.perf_counter() - t0) / reps * 1e6
+    due = {l: frozenset(range(k_pec)) for l in range(L)}
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < 0.5:
+        build_phase_assignment(layout, due, strategy)
+        reps += 1
+    plan_ms = (time.perf_counter() - t0) / reps * 1e3
+    data = rng.integers(0, 256, crc_sample, dtype=np.uint8).tobytes()
+    t0 = time.perf_counter()
+    O.crc32c_py(data)
+    crc_mbs = crc_sample / (time.perf_counter() - t0) / 1e6
+    return {"select_two_tier_us": round(sel_us, 1), "plan_ms": round(plan_ms, 3),
+            "py_crc32c_MBps_1core": round(crc_mbs, 2),
+            "what": "oracle two-tier load-aware selection [L,E]; host planner "
+                    "build_phase_assignment for one due set; reference-style pure-Python "
+                    "CRC-32C on 1 MiB"}
+
+
 # ---------------------------------------------------------------------------
 # exposed checkpoint stall: synthetic training loop with and without PEC
 # ---------------------------------------------------------------------------
@@ -307,6 +345,10 @@ def run_reference(args):
         if i >= args.warmup:
             per_step.append(gbs)
     value = statistics.mean(per_step)
+    try:
+        components = cpu_components(layout, w.strategy, w.pec.k_pec)
+    except Exception as exc:  # reported, never fatal to the line
+        components = {"error": f"{type(exc).__name__}: {exc}"[:200]}
     line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(sample * 1e9 / (value * 1e9) * 1e3, 3),
@@ -317,7 +359,7 @@ def run_reference(args):
                        "parallelism": f"dp{layout.n_ranks}-ep{layout.parallel.ep_degree}",
                        "sample_gb": round(sample, 3)},
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads,
-                             "kind": "port", "sample": desc},
+                             "kind": "port", "sample": desc, "components": components},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -556,6 +598,10 @@ def run_b200(args):
                                     args.cpu_seconds)
         cpu = {"value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",
                "sample": desc}
+        try:
+            cpu["components"] = cpu_components(layout, w.strategy, w.pec.k_pec)
+        except Exception as exc:  # reported, never fatal to the bench line
+            cpu["components"] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
     if rank == 0:
         line = {

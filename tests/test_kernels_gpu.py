@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("L,n,E", [(1, 1, 1), (4, 4096 * 2, 8), (6, 16384 * 2, 8),
                                    (12, 3000, 16), (32, 32768, 8), (3, 100003, 64),
-                                   (2, 77, 4096)])
+                                   (2, 77, 4096), (2, 0, 8)])
 def test_token_hist_matches_bincount_with_cap(dev, L, n, E):
     import torch
     from paper_2408_04307_b200 import device as D

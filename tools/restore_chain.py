@@ -2,8 +2,8 @@
 sweep 1..E on GPT-MoE 350M-16E (dp=ep=8, all 8 ranks emulated on one GPU,
 2 nodes x 4 GPUs).
 
-Chain: sequential K_pec=2 (adaptive plan), one full selection period
-(8 checkpoints), every checkpoint packed, drained and persisted to a
+Chain: sequential K_pec (default 1; adaptive
+plan), one full selection period (16 checkpoints at K=1), every checkpoint packed, drained and persisted to a
 DiskStore on /dev/shm; a stand-in optimizer step perturbs every unit between
 checkpoints so versions differ.  Then node 1 fails: `resolve_recovery`
 decides per unit (memory on node 0 / storage / initial), the state is wiped
@@ -30,6 +30,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 
 def main():
+    import argparse
     import torch
     from paper_2408_04307_b200 import ClusterSpec, PecConfig, build_layout, configs
     from paper_2408_04307_b200 import device as D
@@ -38,9 +39,13 @@ def main():
     from paper_2408_04307_b200.snapshot import PecCheckpointer
     from paper_2408_04307_b200.store import DiskStore
 
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--k", type=int, default=1)
+    ap.add_argument("--verify", default="device", choices=["device", "host"])
+    args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    out = {}
-    w = configs.gpt350m_16e(k_pec=2, strategy="adaptive_pec")
+    out = {"k_pec": args.k, "verify": args.verify}
+    w = configs.gpt350m_16e(k_pec=args.k, strategy="adaptive_pec")
     layout = build_layout(w.model, w.parallel, ClusterSpec(num_nodes=2, gpus_per_node=4))
     arena = StateArena(layout, range(8), dev, w.expert_tensors)
     keys = list(arena.slots)
@@ -55,11 +60,12 @@ def main():
     root = "/dev/shm/pec_chain"
     shutil.rmtree(root, ignore_errors=True)
     store = DiskStore(root, io_threads=16)
-    ck = PecCheckpointer(layout, arena, store, PecConfig(k_pec=2), "adaptive_pec", i_ckpt=1)
+    ck = PecCheckpointer(layout, arena, store, PecConfig(k_pec=args.k), "adaptive_pec",
+                        i_ckpt=1)
     ck.engine.reserve(ck.max_snapshot_bytes())
     fps = {}
     t0 = time.time()
-    period = ck.plan().period  # 8 checkpoints cover every expert once
+    period = ck.plan().period  # E / gcd(E, K) checkpoints cover every expert once
     for it in range(1, period + 1):
         buf = ck.step(it)
         torch.cuda.synchronize()
@@ -85,7 +91,7 @@ def main():
     arena.buffer.zero_()
     torch.cuda.synchronize()
     tr = time.time()
-    rep = restore(ck.engine, plan)
+    rep = restore(ck.engine, plan, verify=args.verify)
     restore_s = time.time() - tr
     now = arena.buffer.cpu().numpy()
     crc_now = dict(zip(keys, (int(c) for c in D.crc32c_many(now, offs, sizes))))
