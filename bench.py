@@ -143,6 +143,20 @@ def sum_over_ranks(x, world, device):
     return float(t.item())
 
 
+def host_buffers_that_fit(nbytes: int, want: int, frac: float = 0.7) -> int:
+    """How many pinned host snapshot buffers of ``nbytes`` each local rank
+    can take (LOCAL_WORLD_SIZE ranks pin at once) within ``frac`` of the
+    node's MemAvailable."""
+    try:
+        with open("/proc/meminfo") as f:
+            info = {ln.split(":")[0]: int(ln.split()[1]) * 1024 for ln in f if ":" in ln}
+        avail = info.get("MemAvailable", info.get("MemFree", 0))
+    except OSError:
+        return want
+    local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    return max(0, min(want, int(frac * avail // (local * max(1, nbytes)))))
+
+
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle's pack restatement on host cores
 # ---------------------------------------------------------------------------
@@ -492,10 +506,24 @@ def run_b200(args):
         # persist tier, 2 without (buffers then recycle through RECOVERY)
         tpin = time.perf_counter()
         pin_error = None
-        try:
-            eng.reserve(eng.staging.numel(), host_buffers=3 if store is not None else 2)
-        except (RuntimeError, MemoryError) as exc:  # e.g. host RAM too small to pin
-            pin_error = f"{type(exc).__name__}: {exc}"[:200]
+        want = 3 if store is not None else 2
+        # never pin more than ~70 % of the node's available RAM (all local
+        # ranks pin at once); every rank uses the node-wide minimum
+        fit = host_buffers_that_fit(eng.staging.numel(), want)
+        n_host = int(-max_over_ranks(-float(fit), world, dev))
+        if n_host < want:
+            print(f"bench: host RAM fits {n_host} of {want} pinned snapshot buffers per rank",
+                  file=sys.stderr)
+        if n_host < 2:
+            args.no_stall = True     # the loop cycles >= 2 buffers
+            args.e2e_steps = 1
+        if n_host < 1:
+            pin_error = "host RAM too small for one pinned snapshot buffer per local rank"
+        else:
+            try:
+                eng.reserve(eng.staging.numel(), host_buffers=n_host)
+            except (RuntimeError, MemoryError) as exc:  # e.g. pinning refused
+                pin_error = f"{type(exc).__name__}: {exc}"[:200]
         pin_s = time.perf_counter() - tpin
         if max_over_ranks(1.0 if pin_error else 0.0, world, dev) > 0:
             # every rank skips the host-buffer legs together (no stranded collectives)
