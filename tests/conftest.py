@@ -58,3 +58,21 @@ def make_layout(n_experts=4, dp=4, ep=2, gpus_per_node=2, **model_kw):
     model = make_model(n_experts=n_experts, **model_kw)
     return build_layout(model, ParallelSpec(dp_degree=dp, ep_degree=ep),
                         make_cluster(dp=dp, gpus_per_node=gpus_per_node))
+
+
+def build_abi_check(out_dir: Path, gpu: bool) -> Path:
+    """Compile tests/c/abi_check.c with gcc against include/pec.h and the
+    in-tree libpec.so (plus the CUDA runtime for the device checks)."""
+    import subprocess
+    from paper_2408_04307_b200 import _build
+    lib = _build.build()
+    exe = out_dir / ("abi_check_gpu" if gpu else "abi_check")
+    cmd = ["gcc", "-O2", "-Wall", "-Wextra", "-Werror", "-std=c11", "-D_DEFAULT_SOURCE",
+           "-I", str(ROOT / "include"), str(ROOT / "tests" / "c" / "abi_check.c"),
+           "-L", str(lib.parent), "-lpec", f"-Wl,-rpath,{lib.parent}", "-o", str(exe)]
+    if gpu:
+        cuda = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+        cmd[1:1] = ["-DPEC_ABI_CHECK_GPU", "-I", str(cuda / "include")]
+        cmd += ["-L", str(cuda / "lib64"), "-lcudart", f"-Wl,-rpath,{cuda / 'lib64'}"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe

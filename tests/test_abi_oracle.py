@@ -115,3 +115,14 @@ def test_native_writer_writes_exact_bytes_and_crcs(tmp_path):
         assert int(c) == crc32c(b)
     with pytest.raises(OSError):
         D.write_files([tmp_path / "missing" / "x.bin"], [bufs[2]])
+
+
+def test_c_abi_host_entry_points_from_plain_c(tmp_path):
+    """include/pec.h compiles as C11 and the host entry points behave as
+    documented when called from C (tests/c/abi_check.c)."""
+    import subprocess
+    from conftest import build_abi_check
+    exe = build_abi_check(tmp_path, gpu=False)
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "0 failure(s)" in res.stdout

@@ -291,3 +291,14 @@ def test_pack_crc_copies_and_checksums_every_entry(dev, congruent):
     got = entry.cpu().numpy().view(np.uint32)
     for (s, _, n), c in zip(copies, got):
         assert int(c) == O.crc32c(host[s:s + n]), (s, n)
+
+
+def test_c_abi_device_entry_points_from_plain_c(dev, tmp_path):
+    """pack / unpack / sequential selection / histogram called from a plain C
+    program through include/pec.h (tests/c/abi_check.c, CUDA runtime)."""
+    import subprocess
+    from conftest import build_abi_check
+    exe = build_abi_check(tmp_path, gpu=True)
+    res = subprocess.run([str(exe), "gpu"], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "0 failure(s)" in res.stdout
