@@ -70,18 +70,6 @@ case "$recipe" in
       --master-addr 127.0.0.1 --master-port 29553 bench.py --impl reference --gpus $N \
       --steps 2 --warmup 1 2>/dev/null | tail -1 > $O/bench_n${N}_ref.json
     ;;
-  sanitize)   # compute-sanitizer over the kernel parity tests and the C ABI program
-    CS="compute-sanitizer --target-processes all --print-limit 20"
-    timeout 1500 $CS --tool memcheck --leak-check no python -m pytest tests/test_kernels_gpu.py -x -q \
-      > $O/sanitize_memcheck.log 2>&1; echo memcheck=$?; tail -3 $O/sanitize_memcheck.log
-    K="token_hist or select or pack_crc or random_ranges or expansion"
-    timeout 1500 $CS --tool racecheck python -m pytest tests/test_kernels_gpu.py -x -q -k "$K" \
-      > $O/sanitize_racecheck.log 2>&1; echo racecheck=$?; tail -3 $O/sanitize_racecheck.log
-    timeout 1500 $CS --tool synccheck python -m pytest tests/test_kernels_gpu.py -x -q -k "$K" \
-      > $O/sanitize_synccheck.log 2>&1; echo synccheck=$?; tail -3 $O/sanitize_synccheck.log
-    timeout 900 $CS --tool initcheck python -m pytest tests/test_kernels_gpu.py -x -q -k "$K" \
-      > $O/sanitize_initcheck.log 2>&1; echo initcheck=$?; tail -3 $O/sanitize_initcheck.log
-    ;;
   *)
     echo "unknown recipe: $recipe" >&2; exit 2 ;;
 esac
