@@ -409,7 +409,7 @@ def run_b200(args):
     if persist != "none":
         base = "/dev/shm" if persist == "shm" else tempfile.gettempdir()
         store_root = tempfile.mkdtemp(prefix="pec_bench_", dir=base)
-        store = DiskStore(store_root, io_threads=8)
+        store = DiskStore(store_root, io_threads=8, direct_io=args.direct_io)
     control = None
     if world > 1 and store is not None:
         import torch.distributed as dist
@@ -601,7 +601,8 @@ def run_b200(args):
         ck.finish()
         if store is not None and eng.stats["persist_s"]:
             persisted = sum(eng.stats["snap_bytes"][-e2e_steps:])
-            persist_info = {"target": persist, "versions": len(eng.stats["persist_s"]),
+            persist_info = {"target": persist, "direct_io": bool(args.direct_io),
+                            "versions": len(eng.stats["persist_s"]),
                             "seconds": [round(x, 2) for x in eng.stats["persist_s"]],
                             "GBps": round(persisted / max(sum(eng.stats["persist_s"]), 1e-9) / 1e9, 2)}
     stall = None
@@ -690,6 +691,8 @@ def main():
     ap.add_argument("--chunk-log2", type=int, default=15)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--persist", default="auto", choices=["auto", "none", "shm", "disk"])
+    ap.add_argument("--direct-io", action="store_true",
+                    help="persist with O_DIRECT (meaningful with --persist disk)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stall", action="store_true")

@@ -17,6 +17,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <atomic>
 #include <thread>
 #include <vector>
@@ -242,6 +244,11 @@ int pec_crc32c_many(const void* base, const uint64_t* offs, const uint64_t* lens
 // is checksummed right after it is written, while it is still cache-hot, so
 // the payload is read once for both.
 // flags bit 0: fsync every file before returning.
+// flags bit 1: O_DIRECT (page-cache bypass for real storage): each piece is
+//   copied into a 4 KiB-aligned per-thread bounce buffer (checksummed there,
+//   cache-hot), the last piece is zero-padded to the 4 KiB block and the file
+//   is truncated back to its exact length.  Filesystems that refuse O_DIRECT
+//   (EINVAL, e.g. tmpfs) get the buffered path for that file.
 int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
                     int n, uint32_t* crc_out, int threads, int flags) {
   if (n < 0 || (n > 0 && (paths == nullptr || bufs == nullptr || lens == nullptr)))
@@ -249,45 +256,79 @@ int pec_write_files(const char* const* paths, const void* const* bufs, const uin
   if (n == 0) return PEC_OK;
   if (threads < 1) threads = 1;
   constexpr uint64_t kPiece = 4ull << 20;
+  constexpr uint64_t kBlock = 4096;
   std::vector<int> order(n);
   for (int i = 0; i < n; ++i) order[i] = i;
   std::sort(order.begin(), order.end(), [&](int a, int b) { return lens[a] > lens[b]; });
   std::atomic<int> next{0};
   std::atomic<int> failed{0};
+  auto write_all = [](int fd, const uint8_t* p, uint64_t len) {
+    uint64_t done = 0;
+    while (done < len) {
+      const ssize_t w = write(fd, p + done, len - done);
+      if (w < 0) {
+        if (errno == EINTR) continue;
+        return false;
+      }
+      done += (uint64_t)w;
+    }
+    return true;
+  };
   auto work = [&]() {
+    uint8_t* bounce = nullptr;  // per-thread, allocated on first O_DIRECT file
     for (int k = next.fetch_add(1); k < n; k = next.fetch_add(1)) {
-      if (failed.load()) return;
+      if (failed.load()) break;
       const int i = order[k];
-      const int fd = open(paths[i], O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
+      const int base = O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC;
+      int fd = -1;
+      bool direct = false;
+      if (flags & 2) {
+        fd = open(paths[i], base | O_DIRECT, 0644);
+        if (fd >= 0) {
+          direct = true;
+        } else if (errno != EINVAL) {
+          failed.store(1);
+          break;
+        }
+      }
+      if (fd < 0) fd = open(paths[i], base, 0644);
       if (fd < 0) {
         failed.store(1);
-        return;
+        break;
+      }
+      if (direct && bounce == nullptr &&
+          posix_memalign(reinterpret_cast<void**>(&bounce), kBlock, kPiece) != 0) {
+        bounce = nullptr;
+        close(fd);
+        failed.store(1);
+        break;
       }
       const uint8_t* src = static_cast<const uint8_t*>(bufs[i]);
       uint32_t crc = 0;
       bool ok = true;
       for (uint64_t off = 0; off < lens[i] && ok; off += kPiece) {
         const uint64_t len = std::min<uint64_t>(kPiece, lens[i] - off);
-        uint64_t done = 0;
-        while (done < len) {
-          const ssize_t w = write(fd, src + off + done, len - done);
-          if (w < 0) {
-            if (errno == EINTR) continue;
-            ok = false;
-            break;
-          }
-          done += (uint64_t)w;
+        if (direct) {
+          std::memcpy(bounce, src + off, len);
+          if (crc_out != nullptr) crc = crc_impl(bounce, len, crc);
+          const uint64_t padded = (len + kBlock - 1) / kBlock * kBlock;
+          if (padded > len) std::memset(bounce + len, 0, padded - len);
+          ok = write_all(fd, bounce, padded);
+        } else {
+          ok = write_all(fd, src + off, len);
+          if (ok && crc_out != nullptr) crc = crc_impl(src + off, len, crc);
         }
-        if (ok && crc_out != nullptr) crc = crc_impl(src + off, len, crc);
       }
+      if (ok && direct && lens[i] % kBlock != 0 && ftruncate(fd, (off_t)lens[i]) != 0) ok = false;
       if (ok && (flags & 1) && fsync(fd) != 0) ok = false;
       if (close(fd) != 0) ok = false;
       if (!ok) {
         failed.store(1);
-        return;
+        break;
       }
       if (crc_out != nullptr) crc_out[i] = crc;
     }
+    free(bounce);
   };
   const int nt = std::min(threads, n);
   std::vector<std::thread> pool;

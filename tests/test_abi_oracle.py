@@ -103,13 +103,19 @@ def test_oracle_pack_unpack_roundtrip():
         assert np.array_equal(back[s:s + n], state[s:s + n])
 
 
-def test_native_writer_writes_exact_bytes_and_crcs(tmp_path):
+@pytest.mark.parametrize("direct,fsync", [(False, False), (True, False), (True, True)])
+def test_native_writer_writes_exact_bytes_and_crcs(tmp_path, direct, fsync):
+    """Buffered and O_DIRECT (bounce buffer, padded last block, truncate
+    back) writes produce the exact bytes and their CRC-32Cs; sizes cover
+    empty, sub-block, block+1 and multi-piece files."""
     from paper_2408_04307_b200 import device as D
     from paper_2408_04307_b200.store import crc32c
     rng = np.random.default_rng(8)
-    bufs = [rng.integers(0, 256, size=n, dtype=np.uint8) for n in (0, 1, 4097, (4 << 20) + 5)]
+    bufs = [rng.integers(0, 256, size=n, dtype=np.uint8)
+            for n in (0, 1, 4096, 4097, (4 << 20) + 5, (8 << 20))]
+    bufs.append(bufs[3][3:])  # unaligned source address
     paths = [tmp_path / f"e{i}.bin" for i in range(len(bufs))]
-    crcs = D.write_files(paths, bufs, threads=3)
+    crcs = D.write_files(paths, bufs, threads=3, direct=direct, fsync=fsync)
     for p, b, c in zip(paths, bufs, crcs):
         assert p.read_bytes() == b.tobytes()
         assert int(c) == crc32c(b)
