@@ -684,7 +684,8 @@ def main():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="mixtral", choices=["toy", "gpt125m", "gpt350m", "mixtral"])
+    ap.add_argument("--workload", default="mixtral",
+                    choices=["toy", "gpt125m", "gpt350m", "gpt350m_la", "mixtral"])
     ap.add_argument("--engine", default="bulk", choices=["vec", "bulk", "crc"],
                     help="pack engine: TMA bulk (default), LDG/STG vector, or vector with "
                          "fused per-entry CRC-32C")
