@@ -237,7 +237,7 @@ def cpu_components(layout, strategy: str, k_pec: int, crc_sample: int = 1 << 20)
 # exposed checkpoint stall: synthetic training loop with and without PEC
 # ---------------------------------------------------------------------------
 
-def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float):
+def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float, rounds: int = 2):
     """Synthetic per-rank training loop on the compute stream: an F&B proxy
     (bf16 8192^3 GEMMs, calibrated to ~fb_ms) then an update proxy (one
     in-place pass over the whole state arena: HBM-bound like a fused Adam
@@ -287,15 +287,23 @@ def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float):
         return t0.elapsed_time(t1) / iters
 
     run(False, 0)  # warm
-    without = run(False, 0)
     n_before = len(ck.engine.stats["pack_ms"])
-    with_ = run(True, 10 ** 6)
-    ck.finish()
+    # alternate without / with (A B A B) so slow drifts (clocks, other
+    # tenants of the host) hit both arms alike; each arm = mean of its runs
+    runs_without, runs_with = [], []
+    for r in range(rounds):
+        runs_without.append(run(False, 0))
+        runs_with.append(run(True, 10 ** 6 * (r + 1)))
+        ck.finish()
+    without, with_ = statistics.mean(runs_without), statistics.mean(runs_with)
     packs = ck.engine.stats["pack_ms"][n_before:]
-    return {"i_ckpt": i_ckpt, "iters": iters, "checkpoints": iters // i_ckpt,
+    return {"i_ckpt": i_ckpt, "iters": iters, "rounds": rounds,
+            "checkpoints": rounds * (iters // i_ckpt),
             "fb_ms": round(n_gemm * gemm_ms, 1), "fb_gemms": n_gemm,
             "update_ms": round(update_ms, 2),
             "iter_ms_without": round(without, 3), "iter_ms_with": round(with_, 3),
+            "runs_ms_without": [round(x, 3) for x in runs_without],
+            "runs_ms_with": [round(x, 3) for x in runs_with],
             "exposed_ms_per_iter": round(with_ - without, 3),
             "pack_ms_in_loop": round(statistics.mean(packs), 3) if packs else None,
             "overhead_frac": round((with_ - without) / without, 5)}
@@ -697,7 +705,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stall", action="store_true")
-    ap.add_argument("--stall-iters", type=int, default=20)
+    ap.add_argument("--stall-iters", type=int, default=30)
     ap.add_argument("--i-ckpt", type=int, default=10)
     ap.add_argument("--fb-ms", type=float, default=100.0)
     ap.add_argument("--cpu-sample-gb", type=float, default=2.0)

@@ -74,6 +74,8 @@ class _Inflight:
     t_begin: float = 0.0
     entry_crc: object = None              # pinned int32 [n] (MODE_CRC)
     crc_keys: object = None
+    pending: object = None                # device plan: (meta, ready) until the drain is enqueued
+    persist_due: object = None            # device plan: persist sets per layer
 
 
 class DeviceCheckpointEngine(CheckpointEngine):
@@ -107,6 +109,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
                                                 thread_name_prefix="pec-persist")
         self._persist: Dict[int, Tuple[Future, List[StoreEntry]]] = {}
         self._abort_persist = threading.Event()
+        self._pending_bid: Optional[int] = None  # device-planned snapshot awaiting its drain
         self.stats = {"pack_ms": [], "drain_ms": [], "persist_s": [], "snap_bytes": []}
 
     # -- buffers -----------------------------------------------------------------
@@ -265,6 +268,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
         import torch
         table, layouts, region, nbytes = self._table_for(assignment, plan_key)
         s = stream or self.pack_stream
+        self.finalize_pending()
         if self._staging_free is not None:
             s.wait_event(self._staging_free)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -276,6 +280,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
     def begin_snapshot(self, iteration: int, checkpoint_index: int,
                        assignment: PhaseAssignment, plan_key=None, compute_stream=None) -> Buffer:
         import torch
+        self.finalize_pending()
         buf = super().begin_snapshot(iteration, checkpoint_index, assignment)
         self._retract_meta(buf.buffer_id)
         try:
@@ -357,32 +362,34 @@ class DeviceCheckpointEngine(CheckpointEngine):
         """Device-only step of a load-aware snapshot: expand + pack, no drain,
         no host synchronisation.  Returns (start_event, end_event)."""
         s = stream or self.pack_stream
+        self.finalize_pending()
         if self._staging_free is not None:
             s.wait_event(self._staging_free)
         _, t0, t1 = self._expand_and_pack(snap_sel_dev, s)
         return t0, t1
 
     def begin_snapshot_device(self, iteration: int, checkpoint_index: int, snap_sel_dev,
-                              persist_sel_dev, compute_stream=None):
+                              persist_sel_dev, compute_stream=None) -> Buffer:
         """Load-aware snapshot from device selections [L, k_s] / [L, k_p]:
-        expand + pack are enqueued at once; the host then waits only for the
-        tiny selection/size copy (not for the pack) to size the drain and to
-        fill the buffer's reference-format content.  Returns (buffer,
-        persist due map)."""
+        expand + pack are enqueued at once, plus a tiny D2H of the staged
+        size and both selections; the call returns without waiting for the
+        GPU.  The drain (whose size the host must know) is enqueued by
+        `finalize_pending` — from `poll`/`snapshot_ready` once that tiny copy
+        has landed, or at the latest by `complete_snapshot` / the next
+        snapshot — which also fills the buffer's reference-format content
+        and its persist sets (`persist_due`)."""
         import torch
-        from .planner import build_phase_assignment
-        rank = self.ranks[0]
+        self.finalize_pending()
         buf = CheckpointEngine.begin_snapshot(self, iteration, checkpoint_index, None)
         self._retract_meta(buf.buffer_id)
         compute = compute_stream or torch.cuda.current_stream(self.device)
-        ps, cs, ms = self.pack_stream, self.copy_stream, self._meta_stream
+        ps, ms = self.pack_stream, self._meta_stream
         ps.wait_stream(compute)
         if self._staging_free is not None:
             ps.wait_event(self._staging_free)
         expanded, t0, t1 = self._expand_and_pack(snap_sel_dev, ps)
         # small D2H of {chunks, bytes} and both selections on a side stream
         ms.wait_event(expanded)
-        L = snap_sel_dev.shape[0]
         meta = torch.empty(2 + snap_sel_dev.numel() + persist_sel_dev.numel(), dtype=torch.int64,
                            pin_memory=True)
         with torch.cuda.stream(ms):
@@ -391,22 +398,44 @@ class DeviceCheckpointEngine(CheckpointEngine):
             meta[2 + snap_sel_dev.numel():].copy_(persist_sel_dev.reshape(-1), non_blocking=True)
         ready = torch.cuda.Event()
         ready.record(ms)
+        rec = _Inflight({}, {self.ranks[0]: 0}, 0, t_begin=time.perf_counter())
+        rec.pack_start, rec.pack_done = t0, t1
+        rec.pending = (meta, ready, snap_sel_dev.shape[0], snap_sel_dev.numel())
+        self._inflight[buf.buffer_id] = rec
+        self._pending_bid = buf.buffer_id
+        return buf
+
+    def finalize_pending(self, block: bool = True) -> bool:
+        """Enqueue the drain of the pending device-planned snapshot (if any)
+        once its size/selection copy has landed (``block=False``: only if it
+        already has).  Returns True when nothing is left pending."""
+        import torch
+        from .planner import build_phase_assignment
+        bid = self._pending_bid
+        if bid is None:
+            return True
+        rec = self._inflight[bid]
+        meta, ready, L, n_snap = rec.pending
+        if not block and not ready.query():
+            return False
         ready.synchronize()
+        rank = self.ranks[0]
+        buf = self.buffers.buffers[bid]
         nbytes = int(meta[1])
-        snap_h = meta[2:2 + snap_sel_dev.numel()].view(L, -1).tolist()
-        pers_h = meta[2 + snap_sel_dev.numel():].view(L, -1).tolist()
+        snap_h = meta[2:2 + n_snap].view(L, -1).tolist()
+        pers_h = meta[2 + n_snap:].view(L, -1).tolist()
         due = {m: frozenset(e for e in snap_h[m] if e >= 0) for m in range(L)}
-        persist_due = {m: frozenset(e for e in pers_h[m] if e >= 0) for m in range(L)}
+        rec.persist_due = {m: frozenset(e for e in pers_h[m] if e >= 0) for m in range(L)}
         assignment = build_phase_assignment(self.layout, due, self.strategy)
         buf.content = assignment
         layout = StagingLayout.build(assignment.get(rank, ()), self.arena, rank)
         if layout.nbytes != nbytes:
             raise RuntimeError(f"device plan ({nbytes} B) disagrees with host plan "
                                f"({layout.nbytes} B)")
-        host = self._ensure_host(buf.buffer_id, nbytes)
-        rec = _Inflight({rank: layout}, {rank: 0}, nbytes, t_begin=time.perf_counter())
-        rec.pack_start, rec.pack_done = t0, t1
-        cs.wait_event(t1)
+        host = self._ensure_host(bid, nbytes)
+        rec.layouts, rec.nbytes = {rank: layout}, nbytes
+        cs = self.copy_stream
+        cs.wait_event(rec.pack_done)
         rec.drain_done = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(cs):
             host[:nbytes].copy_(self.staging[:nbytes], non_blocking=True)
@@ -417,9 +446,19 @@ class DeviceCheckpointEngine(CheckpointEngine):
                 rec.crc_keys = [a.store_key for a in self.template.ranges]
         rec.drain_done.record(cs)
         self._staging_free = rec.drain_done
-        self._inflight[buf.buffer_id] = rec
         self.stats["snap_bytes"].append(layout.payload_bytes)
-        return buf, persist_due
+        rec.pending = None
+        self._pending_bid = None
+        return True
+
+    def persist_due(self, buf: Buffer):
+        """Persist sets of a device-planned snapshot (None for host plans)."""
+        rec = self._inflight.get(buf.buffer_id)
+        if rec is None:
+            return None
+        if rec.pending is not None:
+            self.finalize_pending()
+        return rec.persist_due
 
     def wait_pack(self, buf: Optional[Buffer] = None, stream=None) -> None:
         """Make ``stream`` (default: current) wait for the pack of ``buf`` (or
@@ -433,11 +472,17 @@ class DeviceCheckpointEngine(CheckpointEngine):
 
     def snapshot_ready(self, buf: Buffer) -> bool:
         rec = self._inflight.get(buf.buffer_id)
-        return rec is None or rec.drain_done.query()
+        if rec is None:
+            return True
+        if rec.pending is not None and not self.finalize_pending(block=False):
+            return False
+        return rec.drain_done.query()
 
     def complete_snapshot(self, buf: Buffer) -> Optional[Buffer]:
         rec = self._inflight.get(buf.buffer_id)
         if rec is not None:
+            if rec.pending is not None:
+                self.finalize_pending()
             rec.drain_done.synchronize()
             self.stats["pack_ms"].append(rec.pack_start.elapsed_time(rec.pack_done))
             self.stats["drain_ms"].append(rec.pack_done.elapsed_time(rec.drain_done))
@@ -516,6 +561,11 @@ class DeviceCheckpointEngine(CheckpointEngine):
         torn version has no COMPLETE marker and is ignored by readers."""
         self.pack_stream.synchronize()
         self.copy_stream.synchronize()
+        if self._pending_bid is not None:
+            # a device-planned snapshot whose drain never started: it is
+            # discarded with its SNAPSHOTTING buffer below
+            self._inflight.pop(self._pending_bid, None)
+            self._pending_bid = None
         self._abort_persist.set()
         published = []
         for bid, (fut, _) in self._persist.items():
@@ -537,6 +587,25 @@ class DeviceCheckpointEngine(CheckpointEngine):
             self.host[bid] = None
             shb.close()
         self._shared.clear()
+
+
+class _PersistSelections(dict):
+    """version -> persist sets per layer.  Host-planned checkpoints store
+    theirs at checkpoint time; device-planned (load-aware) ones resolve from
+    the engine on first access."""
+
+    def __init__(self, owner: "PecCheckpointer"):
+        super().__init__()
+        self._owner = owner
+
+    def __missing__(self, version: int):
+        eng = self._owner.engine
+        buf = next((b for b in eng.buffers.buffers if b.version == version), None)
+        due = eng.persist_due(buf) if buf is not None else None
+        if due is None:
+            raise KeyError(version)
+        self[version] = due
+        return due
 
 
 class PecCheckpointer:
@@ -565,7 +634,7 @@ class PecCheckpointer:
                                              shared_host_prefix=shared_host_prefix)
         self.counters = counters
         self.async_persist = async_persist
-        self.persist_sel: Dict[int, Dict[int, frozenset]] = {}
+        self.persist_sel: Dict[int, Dict[int, frozenset]] = _PersistSelections(self)
         self._plan: Optional[ShardPlan] = None
         self.stall_s = 0.0
         self.device_plans = False
@@ -677,8 +746,13 @@ class PecCheckpointer:
             self.stall_s += time.perf_counter() - t0
         snap_d, pers_d = self.counters.select(self.pec.k_snapshot, self.pec.k_persist,
                                               group=self.group)
-        buf, persist_due = self.engine.begin_snapshot_device(iteration, c, snap_d, pers_d)
-        self.persist_sel[buf.version] = persist_due
+        return self.engine.begin_snapshot_device(iteration, c, snap_d, pers_d)
+
+    def resolve(self, buf: Buffer) -> Buffer:
+        """Make a device-planned snapshot's host-side view current (its
+        `content` and persist sets; enqueues its drain if still pending).
+        Host-planned buffers are always current."""
+        self.engine.persist_due(buf)
         return buf
 
     def on_fault(self, failed_nodes) -> None:
@@ -746,6 +820,7 @@ class PecCheckpointer:
         return True
 
     def poll(self) -> None:
+        self.engine.finalize_pending(block=False)
         snapping = self.engine.buffers.snapshotting
         if snapping is not None and self.engine.snapshot_ready(snapping):
             self._complete(snapping)

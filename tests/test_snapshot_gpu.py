@@ -145,6 +145,7 @@ def test_device_load_aware_chain_matches_reference_simulation(dev, tmp_path):
                             for m in range(L)])
             buf = ck.step(i, torch.from_numpy(ids).to(dev))
             if buf is not None:
+                ck.resolve(buf)
                 snap = {m: set() for m in range(L)}
                 for a in buf.content[0]:
                     u = layout.by_key[a.key]
@@ -257,6 +258,7 @@ def test_device_crc_mode_persists_verifiable_versions(dev, tmp_path, selection):
         ids = torch.randint(0, E, (L, 512), dtype=torch.int32, device=dev)
         buf = ck.step(it, ids if counters is not None else None)
         if buf is not None:
+            ck.resolve(buf)  # device-planned: content is filled when the drain is enqueued
             torch.cuda.synchronize()
             expected[buf.version] = _expected_entries(arena.buffer.cpu().numpy(), arena,
                                                       buf.content, [0])

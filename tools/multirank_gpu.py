@@ -90,6 +90,7 @@ def main():
             glob[1] += c
         buf = ck.step(it, torch.from_numpy(ids[rank]).to(dev))
         if buf is not None:
+            ck.resolve(buf)
             ss, ps, glob[0], glob[1] = O.two_tier_load_aware(glob[0], glob[1], 2, 1)
             got_p = [sorted(ck.persist_sel[buf.version][m]) for m in range(L)]
             ok &= got_p == ps
