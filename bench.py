@@ -237,6 +237,16 @@ def cpu_components(layout, strategy: str, k_pec: int, crc_sample: int = 1 << 20)
 # exposed checkpoint stall: synthetic training loop with and without PEC
 # ---------------------------------------------------------------------------
 
+def prune_store(store, keep: int = 1) -> None:
+    """Bench-only retention: drop all but the newest ``keep`` complete
+    versions (each is a full rank shard; /dev/shm is host RAM)."""
+    if store is None or not hasattr(store, "version_dir"):
+        return
+    import shutil
+    for v in store.complete_versions()[:-keep]:
+        shutil.rmtree(store.version_dir(v), ignore_errors=True)
+
+
 def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float, rounds: int = 2):
     """Synthetic per-rank training loop on the compute stream: an F&B proxy
     (bf16 8192^3 GEMMs, calibrated to ~fb_ms) then an update proxy (one
@@ -295,6 +305,7 @@ def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float, rounds:
         runs_without.append(run(False, 0))
         runs_with.append(run(True, 10 ** 6 * (r + 1)))
         ck.finish()
+        prune_store(ck.engine.store)
     without, with_ = statistics.mean(runs_without), statistics.mean(runs_with)
     packs = ck.engine.stats["pack_ms"][n_before:]
     return {"i_ckpt": i_ckpt, "iters": iters, "rounds": rounds,
@@ -615,6 +626,7 @@ def run_b200(args):
                             "GBps": round(persisted / max(sum(eng.stats["persist_s"]), 1e-9) / 1e9, 2)}
     stall = None
     if not args.no_stall:
+        prune_store(store)
         stall = measure_stall(ck, arena, dev, args.stall_iters, args.i_ckpt, args.fb_ms)
         stall["exposed_ms_per_iter"] = round(max_over_ranks(stall["exposed_ms_per_iter"],
                                                             world, dev), 3)
