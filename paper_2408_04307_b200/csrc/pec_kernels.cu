@@ -604,7 +604,7 @@ struct Geometry {
   int smem = 0;
 };
 
-template <int kStages, int kSLog2, bool kHint, int kMaxPerSM = 64>
+template <int kStages, int kSLog2, bool kHint, int kMaxPerSM = 64, int kGridDiv = 1>
 int launch_bulk(const pec_copy_desc* descs, int n, uint64_t total, const uint64_t* total_dev,
                 int lg, cudaStream_t st) {
   static Geometry geo[64];
@@ -620,7 +620,8 @@ int launch_bulk(const pec_copy_desc* descs, int n, uint64_t total, const uint64_
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBulkThreads, g.smem);
     if (per_sm > kMaxPerSM) per_sm = kMaxPerSM;
-    g.grid = sm_count() * (per_sm < 1 ? 1 : per_sm);
+    const int sms = sm_count() / kGridDiv;  // narrow variants leave SMs to co-running kernels
+    g.grid = (sms < 1 ? 1 : sms) * (per_sm < 1 ? 1 : per_sm);
     g.ready = 1;
   }
   const int smem = kStages << (lg < kSLog2 ? lg : kSLog2);
@@ -647,11 +648,12 @@ int launch_vec(const pec_copy_desc* descs, int n, uint64_t total, const uint64_t
 }
 
 // mode 1: vector engine; 2: TMA bulk engine (the default); 10-16: bulk-engine
-// ring/occupancy variants kept for benchmarking (tools/pack_variants.py).
+// ring/occupancy variants, 17-20: on 1/2 .. 1/8 of the SMs, kept for
+// benchmarking (tools/pack_variants.py, tools/overlap_probe.py).
 int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, const uint64_t* total_dev,
                 int lg, int mode, void* stream) {
   if (n < 0 || lg < 12 || lg > 24) return PEC_E_INVAL;
-  const bool known = (mode >= 0 && mode <= 2) || (mode >= 10 && mode <= 16);
+  const bool known = (mode >= 0 && mode <= 2) || (mode >= 10 && mode <= 20);
   if (!known) return PEC_E_INVAL;
   if (total == 0 || n == 0) return PEC_OK;
   if (descs == nullptr) return PEC_E_INVAL;
@@ -665,6 +667,11 @@ int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, const uint64_
     case 14: return launch_bulk<3, 15, true, 1>(descs, n, total, total_dev, lg, st);
     case 15: return launch_bulk<2, 16, false, 1>(descs, n, total, total_dev, lg, st);
     case 16: return launch_bulk<6, 15, false, 1>(descs, n, total, total_dev, lg, st);
+    // narrow: a fraction of the SMs (overlap studies with co-running training kernels)
+    case 17: return launch_bulk<3, 15, true, 1, 2>(descs, n, total, total_dev, lg, st);
+    case 18: return launch_bulk<3, 15, true, 1, 4>(descs, n, total, total_dev, lg, st);
+    case 19: return launch_bulk<6, 15, true, 1, 4>(descs, n, total, total_dev, lg, st);
+    case 20: return launch_bulk<6, 15, true, 1, 8>(descs, n, total, total_dev, lg, st);
     // default (measured best on B200, tools/pack_variants.py): one CTA per
     // SM, 3 x 32 KiB stages (two loads in flight while one stage drains),
     // L2 evict_first on both directions (streamed once; keeps L2 for the
