@@ -195,6 +195,17 @@ def cpu_pack_sample(entries, sample_bytes: int, threads: int, min_seconds: float
     return payload * reps / dt / 1e9, desc
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_components(layout, strategy: str, k_pec: int, crc_sample: int = 1 << 20):
     """The reference's other per-checkpoint CPU costs:
     two-tier load-aware selection (oracle restatement of the reference's
@@ -392,7 +403,8 @@ def run_reference(args):
                        "parallelism": f"dp{layout.n_ranks}-ep{layout.parallel.ep_degree}",
                        "sample_gb": round(sample, 3)},
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads,
-                             "kind": "port", "sample": desc, "components": components},
+                             "kind": "port", "sample": desc, "cpu_model": cpu_model(),
+                             "components": components},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -646,7 +658,7 @@ def run_b200(args):
         gbs, desc = cpu_pack_sample(first_layout.entries, int(args.cpu_sample_gb * 1e9), threads,
                                     args.cpu_seconds)
         cpu = {"value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": desc}
+               "sample": desc, "cpu_model": cpu_model()}
         try:
             cpu["components"] = cpu_components(layout, w.strategy, w.pec.k_pec)
         except Exception as exc:  # reported, never fatal to the bench line
