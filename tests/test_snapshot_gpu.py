@@ -228,6 +228,67 @@ def test_fault_mid_snapshot_and_mid_persist_leaves_consistent_state(dev, tmp_pat
     ck.close()
 
 
+def test_load_aware_pending_drain_survives_faults_and_poll_order(dev, tmp_path):
+    """Device-planned (load-aware) snapshots return before the host knows
+    their size: a fault while the drain is still pending discards the
+    snapshot cleanly; poll() later enqueues pending drains without blocking;
+    the persisted bytes and a restore stay exact."""
+    import torch
+    from paper_2408_04307_b200 import PecConfig, configs
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.counting import DeviceTokenCounters
+    from paper_2408_04307_b200.engine import FREE
+    from paper_2408_04307_b200.restore import restore
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore
+    w = configs.toy()
+    layout = w.layout()
+    L, E = layout.model.num_moe_layers, layout.model.experts_per_layer
+    arena = StateArena(layout, [0], dev, w.expert_tensors)
+    store = DiskStore(tmp_path)
+    counters = DeviceTokenCounters(L, E, dev)
+    pec = PecConfig(k_pec=2, selection="load_aware", k_snapshot=2, k_persist=1)
+    ck = PecCheckpointer(layout, arena, store, pec, "equal_pec", i_ckpt=1, counters=counters)
+    ck.engine.reserve(ck.max_snapshot_bytes())
+    gen = torch.Generator(device=dev).manual_seed(5)
+
+    def ids():
+        return torch.randint(0, E, (L, 256), dtype=torch.int32, device=dev, generator=gen)
+
+    b1 = ck.step(1, ids())
+    assert b1.content is None                 # plan still on the GPU
+    ck.engine.on_fault(set())                 # drain never enqueued: discarded
+    assert b1.status == FREE and ck.engine._pending_bid is None
+    expected = {}
+    for it in range(2, 7):
+        _mutate(arena, it)
+        buf = ck.step(it, ids())
+        torch.cuda.synchronize()
+        ck.poll()                             # the size copy has landed: drain enqueued
+        assert buf.content is not None
+        expected[buf.version] = _expected_entries(arena.buffer.cpu().numpy(), arena,
+                                                  buf.content, [0])
+        ck.wait_pack()
+    ck.finish()
+    assert store.complete_versions() == sorted(expected)
+    for v in store.complete_versions():
+        got = store.load_checkpoint(v)
+        for sk, data in got.items():
+            assert data == expected[v][sk], (v, sk)
+    torch.cuda.synchronize()
+    good = arena.buffer.cpu().numpy().copy()
+    plan = ck.engine.resolve_recovery(set())
+    arena.buffer.zero_()
+    restore(ck.engine, plan)
+    got_state = arena.buffer.cpu().numpy()
+    for key, d in plan.decisions.items():
+        if d.source != "initial" and d.restored_iteration == 6:
+            sl = arena.slots[key]
+            assert np.array_equal(got_state[sl.offset:sl.offset + sl.size],
+                                  good[sl.offset:sl.offset + sl.size]), key
+    ck.close()
+
+
 @pytest.mark.parametrize("selection", ["sequential", "load_aware"])
 def test_device_crc_mode_persists_verifiable_versions(dev, tmp_path, selection):
     """MODE_CRC: the pack computes every entry's CRC-32C; the persist writes
