@@ -318,6 +318,10 @@ class DiskStore:
         meta = self.meta(version)
         ents = {}
         for line in (vdir / "manifest.tsv").read_text().splitlines():
+            if not line:
+                # an entry-less version's manifest is "\n"; the reference's
+                # reader fails on it (store.py:251-252), this one reads {}
+                continue
             k, p, s, c = line.split("\t")
             ents[k] = (p, int(s), int(c, 16))
         return StoreManifest(version, meta.iteration, ents, True)
