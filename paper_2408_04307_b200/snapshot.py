@@ -64,6 +64,17 @@ class PersistAborted(RuntimeError):
 
 
 @dataclass
+class RecoveryOutcome:
+    """What `PecCheckpointer.recover` did (the byte-moving counterpart of the
+    reference's `_handle_fault` bookkeeping, simulator.py:473-544)."""
+    restart_iteration: int        # resume training at restart_iteration + 1
+    version_skew: int
+    plan: object                  # RecoveryPlan, or None for a restart from scratch
+    report: object                # RestoreReport, or None
+    expert_restore: Dict[Tuple[int, int], int]   # (layer, expert) -> restored iteration
+
+
+@dataclass
 class _Inflight:
     """Device-side record of one buffer's snapshot."""
     layouts: Dict[int, StagingLayout]     # local rank -> layout (offsets within its region)
@@ -637,6 +648,10 @@ class PecCheckpointer:
         self.persist_sel: Dict[int, Dict[int, frozenset]] = _PersistSelections(self)
         self._plan: Optional[ShardPlan] = None
         self.stall_s = 0.0
+        # cumulative delivered tokens of the current timeline at every
+        # checkpoint iteration (for the counter reset after a recovery)
+        self._cum_at: Dict[int, object] = {}
+        self._replay_offset = None
         self.device_plans = False
         if pec is not None and pec.selection == LOAD_AWARE:
             if strategy == ADAPTIVE_PEC:
@@ -701,8 +716,17 @@ class PecCheckpointer:
             return self.checkpoint(iteration)
         return None
 
+    def _timeline_delivered(self):
+        import torch
+        d = self.counters.delivered
+        if self._replay_offset is None:
+            self._replay_offset = torch.zeros_like(d)
+        return d - self._replay_offset
+
     def checkpoint(self, iteration: int) -> Buffer:
         c = iteration // self.i_ckpt - 1
+        if self.counters is not None:
+            self._cum_at[iteration] = self._timeline_delivered()
         if self.device_plans:
             return self._checkpoint_device(iteration, c)
         snap_sel, persist_sel = self.selections(c)
@@ -763,6 +787,77 @@ class PecCheckpointer:
             nxt = self.engine.buffers.promote_if_idle()
             if nxt is not None:
                 self._start_persist(nxt)
+
+    def recover(self, failed_nodes, iteration: int, verify: str = "device") -> RecoveryOutcome:
+        """Full fault handling with real bytes, in the reference's order
+        (`Simulation._handle_fault`, simulator.py:473-544): resolve the
+        newest source of every unit (capped at ``iteration``), unwind
+        in-flight work (`on_fault`, resuming an interrupted persist from
+        surviving memory), move the bytes back into the state arena
+        (`restore`: memory / storage / initial), and reset both load-aware
+        counter tiers to the tokens each expert received between its restored
+        iteration and the restart point (simulator.py:527-532).  With no
+        COMPLETE version the run restarts from scratch: every unit is
+        re-initialised and the buffers are dropped (simulator.py:476-483).
+        The caller resumes training at ``restart_iteration + 1``."""
+        from .restore import restore
+        failed = frozenset(failed_nodes)
+        L, E = self.layout.model.num_moe_layers, self.layout.model.experts_per_layer
+        store = self.engine.store
+        # unwind in-flight work first: a persist that already published is
+        # honoured, one that had not is discarded (no COMPLETE).  The
+        # decisions below equal the reference's taken before on_fault: the
+        # cleared SNAPSHOTTING buffer was no source, PERSISTING ->
+        # SNAPSHOTTED stays one, failed nodes are excluded either way.
+        self.engine.on_fault(failed)
+        if store is None or store.newest_complete() is None:
+            for b in self.engine.buffers.buffers:
+                b.clear()
+            for key in list(self.arena.slots):
+                self.arena.fill_unit(key)
+            plan = report = None
+            restart, skew = 0, 0
+            expert_restore = {(m, e): 0 for m in range(L) for e in range(E)}
+        else:
+            plan = self.engine.resolve_recovery(failed, max_iteration=iteration)
+            if self.engine.buffers.persisting is None:   # resume a cut-off persist
+                nxt = self.engine.buffers.promote_if_idle()
+                if nxt is not None:
+                    self._start_persist(nxt)
+            report = restore(self.engine, plan, verify=verify)
+            restart, skew = plan.restart_iteration, plan.version_skew
+            expert_restore = {}
+            for m in range(L):
+                for e in range(E):
+                    wd = plan.decisions.get(f"ew.L{m}.E{e}")
+                    od = plan.decisions.get(f"eo.L{m}.E{e}")
+                    expert_restore[(m, e)] = restart if wd is None or od is None else \
+                        min(wd.restored_iteration, od.restored_iteration)
+        if self.counters is not None:
+            self._reset_counters(expert_restore, restart)
+        return RecoveryOutcome(restart, skew, plan, report, expert_restore)
+
+    def _reset_counters(self, expert_restore: Dict[Tuple[int, int], int], restart: int) -> None:
+        """unsaved(m, e) = tokens delivered in (restored(m, e), restart], from
+        the cumulative-delivered snapshots taken at checkpoints; the
+        timeline then rewinds to the restart point (replayed iterations are
+        counted again)."""
+        import torch
+        timeline = self._timeline_delivered()
+        zero = torch.zeros_like(timeline)
+        base = self._cum_at.get(restart, zero) if restart else zero
+        unsaved = torch.zeros_like(timeline)
+        restored = torch.tensor([[expert_restore[(m, e)] for e in range(timeline.shape[1])]
+                                 for m in range(timeline.shape[0])], device=timeline.device)
+        for r in sorted(set(expert_restore.values())):
+            if r >= restart:
+                continue
+            at_r = self._cum_at.get(r, zero) if r else zero
+            mask = restored == r
+            unsaved[mask] = (base - at_r)[mask]
+        self.counters.reset_to(unsaved, unsaved)
+        self._replay_offset = self.counters.delivered - base
+        self._cum_at = {k: v for k, v in self._cum_at.items() if k <= restart}
 
     def wait_pack(self, stream=None) -> None:
         self.engine.wait_pack(stream=stream)

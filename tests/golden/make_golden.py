@@ -175,6 +175,67 @@ def gen_loadaware_sim():
     return {"traces": traces}
 
 
+def gen_fault_sim():
+    """Reference Simulation with load-aware selection on 2 nodes and scripted
+    node faults: per-checkpoint selections (including the checkpoints of
+    replayed iterations), and for every fault the recovery decisions, the
+    restart point / skew and both counter tiers after the reset
+    (simulator.py:473-544) -- drives parity of PecCheckpointer.recover."""
+    from mocsim.scenario import FaultSpec
+    traces = []
+    for L, E, tokens, k_s, k_p, seed, events in [
+            (3, 4, 600, 2, 1, 5, ((13, (1,)), (27, (0,)))),
+            (2, 8, 800, 2, 2, 9, ((8, (1,)), (21, (1,)), (33, (0,))))]:
+        model = mocsim.ModelSpec(num_moe_layers=L, experts_per_layer=E, top_k=2,
+                                 non_expert_params=1000, expert_params_per_expert=100,
+                                 bytes_weight=2, bytes_optim=12)
+        pec = mocsim.PecConfig(k_pec=k_s, selection="load_aware", k_snapshot=k_s,
+                               k_persist=k_p)
+        sc = Scenario(model=model, parallel=mocsim.ParallelSpec(2, 2),
+                      cluster=ref_cluster(2, 1), strategy="equal_pec", i_ckpt=5,
+                      i_total=40, rng_seed=seed, tokens_per_iteration=tokens, pec=pec,
+                      routing=RoutingSpec(kind="zipf", zipf_s=1.1), capacity_factor=1.25,
+                      faults=FaultSpec(kind="scripted", events=events))
+        sim = mocsim.Simulation(sc)
+        rec, faults = [], []
+        orig_sel, orig_fault = sim._selections, sim._handle_fault
+
+        def spy(c, tiers, _orig=orig_sel, _rec=rec):
+            snap, persist = _orig(c, tiers)
+            _rec.append({"c": c, "snap": [sorted(snap[m]) for m in sorted(snap)],
+                         "persist": [sorted(persist[m]) for m in sorted(persist)]})
+            return snap, persist
+
+        def fault_spy(iteration, failed, _orig=orig_fault, _sim=sim, _faults=faults):
+            plan = None
+            if _sim.store.newest_complete() is not None:
+                plan = _sim.engine.resolve_recovery(failed, max_iteration=iteration)
+            _orig(iteration, failed)
+            fr = _sim.fault_records[-1]
+            _faults.append({
+                "iteration": iteration, "failed": sorted(failed),
+                "restart": fr.restart_iteration, "skew": fr.version_skew,
+                "decisions": None if plan is None else {
+                    k: [d.source, d.node, d.version, d.restored_iteration]
+                    for k, d in sorted(plan.decisions.items())},
+                "snap_counters": [[_sim.snap_counters.unsaved_tokens[(m, e)] for e in range(E)]
+                                  for m in range(L)],
+                "persist_counters": [[_sim.persist_counters.unsaved_tokens[(m, e)]
+                                      for e in range(E)] for m in range(L)]})
+        sim._selections = spy
+        sim._handle_fault = fault_spy
+        n_steps = 0
+        while sim.next_iteration <= sc.i_total and n_steps < 500:
+            sim.step()
+            n_steps += 1
+        traces.append({"layers": L, "experts": E, "tokens": tokens, "top_k": 2,
+                       "k_snapshot": k_s, "k_persist": k_p, "zipf_s": 1.1,
+                       "capacity_factor": 1.25, "seed": seed, "i_ckpt": 5, "i_total": 40,
+                       "events": [[it, list(n)] for it, n in events],
+                       "checkpoints": rec, "faults": faults})
+    return {"traces": traces}
+
+
 def gen_plans():
     out = {"workloads": {}, "small": []}
     wl = {"toy": configs.toy(), "gpt125m": configs.gpt125m_8e(),
@@ -363,7 +424,8 @@ def gen_policy():
 def main():
     HERE.mkdir(exist_ok=True)
     for name, fn in [("routing", gen_routing), ("selection", gen_selection),
-                     ("loadaware_sim", gen_loadaware_sim), ("plans", gen_plans),
+                     ("loadaware_sim", gen_loadaware_sim), ("fault_sim", gen_fault_sim),
+                     ("plans", gen_plans),
                      ("store", gen_store), ("recovery", gen_recovery),
                      ("policy", gen_policy)]:
         doc = fn()

@@ -158,6 +158,111 @@ def test_device_load_aware_chain_matches_reference_simulation(dev, tmp_path):
         assert got == t["checkpoints"]
 
 
+def test_recover_matches_reference_fault_simulation(dev, tmp_path):
+    """PecCheckpointer.recover reproduces the reference's fault handling
+    (Simulation._handle_fault, simulator.py:473-544) on a 2-node load-aware
+    run with scripted node faults (golden trace): the recovery decisions,
+    restart point and skew of every fault, both counter tiers after the
+    reset, and every checkpoint's selections before and after (including
+    replayed iterations) -- with the bytes actually restored."""
+    import json
+    import torch
+    from conftest import GOLDEN
+    from paper_2408_04307_b200 import (ClusterSpec, ModelSpec, ParallelSpec, PecConfig,
+                                       build_layout)
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.counting import DeviceTokenCounters
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore
+    g = json.loads((GOLDEN / "fault_sim.json").read_text())
+    for ti, t in enumerate(g["traces"]):
+        L, E = t["layers"], t["experts"]
+        model = ModelSpec(num_moe_layers=L, experts_per_layer=E, top_k=t["top_k"],
+                          non_expert_params=1000, expert_params_per_expert=100,
+                          bytes_weight=2, bytes_optim=12)
+        layout = build_layout(model, ParallelSpec(2, 2), ClusterSpec(2, 1))
+        arena = StateArena(layout, [0, 1], dev)
+        total = t["tokens"] * t["top_k"]
+        counters = DeviceTokenCounters(
+            L, E, dev, DeviceTokenCounters.capacity_for(t["capacity_factor"], [total] * L, E))
+        pec = PecConfig(k_pec=t["k_snapshot"], selection="load_aware",
+                        k_snapshot=t["k_snapshot"], k_persist=t["k_persist"])
+        ck = PecCheckpointer(layout, arena, DiskStore(tmp_path / f"t{ti}"), pec, "equal_pec",
+                             i_ckpt=t["i_ckpt"], counters=counters)
+        events = {it: set(n) for it, n in t["events"]}
+        got_ckpts, got_faults = [], []
+        it, steps = 1, 0
+        while it <= t["i_total"] and steps < 500:
+            steps += 1
+            ids = np.stack([O.zipf_router_ids(t["seed"], it, m, E, total, t["zipf_s"])
+                            for m in range(L)])
+            buf = ck.step(it, torch.from_numpy(ids).to(dev))
+            if buf is not None:
+                ck.resolve(buf)
+                snap = {m: set() for m in range(L)}
+                for ranges in buf.content.values():
+                    for a in ranges:
+                        u = layout.by_key[a.key]
+                        if u.layer is not None:
+                            snap[u.layer].add(u.expert)
+                got_ckpts.append({"c": buf.checkpoint_index,
+                                  "snap": [sorted(snap[m]) for m in range(L)],
+                                  "persist": [sorted(ck.persist_sel[buf.version][m])
+                                              for m in range(L)]})
+                ck.wait_pack()
+            if it in events:
+                ck.finish()  # the reference's tiny persists have landed by now
+                out = ck.recover(events.pop(it), it)
+                torch.cuda.synchronize()
+                cnt = counters.counts.cpu().tolist()
+                got_faults.append({
+                    "restart": out.restart_iteration, "skew": out.version_skew,
+                    "decisions": None if out.plan is None else {
+                        k: [d.source, d.node, d.version, d.restored_iteration]
+                        for k, d in sorted(out.plan.decisions.items())},
+                    "snap_counters": cnt[0], "persist_counters": cnt[1]})
+                assert out.report is None or out.report.units == len(arena.slots)
+                it = out.restart_iteration + 1
+            else:
+                it += 1
+        ck.close()
+        want = [{k: f[k] for k in ("restart", "skew", "decisions", "snap_counters",
+                                   "persist_counters")} for f in t["faults"]]
+        assert got_faults == want, ti
+        assert got_ckpts == t["checkpoints"], ti
+
+
+def test_recover_before_any_complete_version_restarts_from_scratch(dev, tmp_path):
+    """No COMPLETE version yet: restart iteration 0, every unit back to its
+    initial image, buffers dropped, counters zeroed (simulator.py:476-483)."""
+    import torch
+    from paper_2408_04307_b200 import PecConfig, configs
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.counting import DeviceTokenCounters
+    from paper_2408_04307_b200.engine import FREE
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore
+    w = configs.toy()
+    layout = w.layout()
+    L, E = layout.model.num_moe_layers, layout.model.experts_per_layer
+    arena = StateArena(layout, [0], dev, w.expert_tensors)
+    initial = arena.buffer.cpu().numpy().copy()
+    counters = DeviceTokenCounters(L, E, dev)
+    pec = PecConfig(k_pec=1, selection="load_aware")
+    ck = PecCheckpointer(layout, arena, DiskStore(tmp_path), pec, "equal_pec", i_ckpt=5,
+                         counters=counters)
+    for it in range(1, 4):
+        _mutate(arena, it)
+        ck.step(it, torch.randint(0, E, (L, 128), dtype=torch.int32, device=dev))
+    out = ck.recover({0}, 3)
+    torch.cuda.synchronize()
+    assert out.restart_iteration == 0 and out.plan is None
+    assert np.array_equal(arena.buffer.cpu().numpy(), initial)
+    assert int(counters.counts.abs().sum()) == 0
+    assert all(b.status == FREE for b in ck.engine.buffers.buffers)
+    ck.close()
+
+
 @pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
 def test_gpt350m_k_sweep_pack_bit_exact_on_device(dev, k):
     """K_pec sweep on GPT-MoE 350M-16E (dp=8 x ep=8, ranks 0..7 emulated):
