@@ -7,8 +7,11 @@ GPT-MoE 350M-16E, dp=ep=N deployment (N = world size), K_pec=2 load-aware
     on every rank == the oracle's selection on the summed counts,
   * pack + drain + multi-writer persist (gloo control group) to a shared store,
   * every rank verifies its persisted entries against its arena bytes,
-then a storage restore of every rank's units after wiping them is checked
-bit-exact.  Prints one JSON line per rank; exits non-zero on any mismatch.
+then node N-1 fails: `PecCheckpointer.recover` on every rank (identical
+decisions; memory / storage / initial bytes back into the wiped arena, checked
+bit-exact per unit; the all-reduced counters after the reset equal the global
+tokens delivered between each expert's restored iteration and the restart
+point).  Prints one JSON line per rank; exits non-zero on any mismatch.
 """
 
 import json
@@ -45,7 +48,6 @@ def main():
     from paper_2408_04307_b200 import PecConfig, configs
     from paper_2408_04307_b200.arena import StateArena
     from paper_2408_04307_b200.counting import DeviceTokenCounters
-    from paper_2408_04307_b200.restore import restore
     from paper_2408_04307_b200.snapshot import PecCheckpointer
     from paper_2408_04307_b200.store import DiskStore, crc32c
 
@@ -81,13 +83,16 @@ def main():
     ok = True
     persisted_bytes = {}
     t0 = time.time()
+    delivered = {}  # iteration -> global delivered counts [L, E]
     for it in range(1, 10):
         ids = {r: np.stack([O.zipf_router_ids(100 + r, it, m, E, routed, 1.1) for m in range(L)])
                for r in range(world)}
+        delivered[it] = np.zeros((L, E), dtype=np.int64)
         for r in range(world):
             c = O.route_counts(ids[r], E, cap)
             glob[0] += c
             glob[1] += c
+            delivered[it] += c
         buf = ck.step(it, torch.from_numpy(ids[rank]).to(dev))
         if buf is not None:
             ck.resolve(buf)
@@ -123,12 +128,19 @@ def main():
     # node `world-1` fails: every rank restores all of its resident units from
     # memory (own or a surviving peer's node-shared buffer), storage or initial
     failed = {world - 1}
-    plan = ck.engine.resolve_recovery(failed)
-    ck.engine.on_fault(failed)
-    keys = [k for k in plan.decisions if arena.has(k)]
     arena.buffer.zero_()
-    rep = restore(ck.engine, plan, keys=keys)
+    out = ck.recover(failed, 9)       # decisions -> unwind -> restore -> counter reset
+    plan, rep = out.plan, out.report
+    keys = [k for k in plan.decisions if arena.has(k)]
     after = arena.buffer.cpu().numpy()
+    # global unsaved tokens after the reset: delivered in (restored, restart]
+    want_unsaved = np.zeros((L, E), dtype=np.int64)
+    for (m, e), r in out.expert_restore.items():
+        if r < out.restart_iteration:
+            want_unsaved[m, e] = sum(delivered[i][m, e]
+                                     for i in range(r + 1, out.restart_iteration + 1))
+    got = counters.all_reduced(dist.group.WORLD).cpu().numpy()
+    counters_ok = bool(np.array_equal(got[0], want_unsaved) and np.array_equal(got[1], want_unsaved))
     restore_ok = bool(keys)
     sources = {}
     for k in keys:
@@ -141,7 +153,8 @@ def main():
     dist.barrier()  # peers may still be reading this rank's shared buffers
     ck.close()
     res = {"rank": rank, "world": world, "selection_ok": bool(sel_ok), "files_ok": bool(files_ok),
-           "restore_ok": bool(restore_ok), "versions": versions, "restored_units": len(keys),
+           "restore_ok": bool(restore_ok), "counters_ok": counters_ok,
+           "restart": out.restart_iteration, "versions": versions, "restored_units": len(keys),
            "sources": sources, "memory_bytes": rep.memory_bytes,
            "storage_bytes": rep.storage_bytes, "restore_wall_s": round(rep.wall_s, 2),
            "seconds": round(time.time() - t0, 1)}
@@ -151,7 +164,7 @@ def main():
         import shutil
         shutil.rmtree(root, ignore_errors=True)
     dist.destroy_process_group()
-    return 0 if (sel_ok and files_ok and restore_ok) else 1
+    return 0 if (sel_ok and files_ok and restore_ok and counters_ok) else 1
 
 
 if __name__ == "__main__":
