@@ -603,14 +603,11 @@ def run_b200(args):
             if hb is not None:
                 n_ = min(hb.numel(), eng.staging.numel())
                 hb[:n_].copy_(eng.staging[:n_])
-        barrier(world)
-        torch.cuda.synchronize()
         h2d = d2h = 0
         base_it = args.warmup + args.steps + 10
-        ck.hold_persist(True)   # measure the snapshot tier alone; persist after
-        tw = time.perf_counter()
-        for k in range(e2e_steps):
-            it = base_it + k
+
+        def e2e_step(k, it):
+            nonlocal h2d, d2h
             ids_dev.copy_(ids_host[k], non_blocking=True)
             h2d += ids_host[k].numel() * 4
             counters.add_iteration(ids_dev)
@@ -619,6 +616,19 @@ def run_b200(args):
             first = eng.snapshot_layout(buf, rank).entries[0]
             _ = int(eng.entry_view(buf, rank, first.store_key)[0])  # host read
             d2h += eng.snapshot_nbytes(buf)
+
+        # one untimed step through the same calls (first-call host costs), then
+        # its persist drains before the timed steps
+        e2e_step(e2e_steps, base_it - args.i_ckpt)
+        ck.finish()
+        h2d = d2h = 0
+        n_persist0 = len(eng.stats["persist_s"])
+        barrier(world)
+        torch.cuda.synchronize()
+        ck.hold_persist(True)   # measure the snapshot tier alone; persist after
+        tw = time.perf_counter()
+        for k in range(e2e_steps):
+            e2e_step(k, base_it + k)
         e2e_s = time.perf_counter() - tw
         e2e_s = max_over_ranks(e2e_s, world, dev)
         e2e_moved = sum_over_ranks(sum(eng.stats["snap_bytes"][-e2e_steps:]), world, dev)
@@ -630,12 +640,13 @@ def run_b200(args):
                "host_pin_s": round(pin_s, 1)}
         tp0 = time.perf_counter()
         ck.finish()
-        if store is not None and eng.stats["persist_s"]:
+        timed_persist = eng.stats["persist_s"][n_persist0:]
+        if store is not None and timed_persist:
             persisted = sum(eng.stats["snap_bytes"][-e2e_steps:])
             persist_info = {"target": persist, "direct_io": bool(args.direct_io),
-                            "versions": len(eng.stats["persist_s"]),
-                            "seconds": [round(x, 2) for x in eng.stats["persist_s"]],
-                            "GBps": round(persisted / max(sum(eng.stats["persist_s"]), 1e-9) / 1e9, 2)}
+                            "versions": len(timed_persist),
+                            "seconds": [round(x, 2) for x in timed_persist],
+                            "GBps": round(persisted / max(sum(timed_persist), 1e-9) / 1e9, 2)}
     stall = None
     if not args.no_stall:
         prune_store(store)
