@@ -263,6 +263,65 @@ def test_recover_before_any_complete_version_restarts_from_scratch(dev, tmp_path
     ck.close()
 
 
+@pytest.mark.parametrize("engine", ["bulk", "crc"])
+def test_mixtral_rank_full_size_pack_unpack_bit_exact(dev, engine):
+    """The headline configuration at full size (Mixtral-shaped rank 0, 84.5 GB
+    resident, every phase of the adaptive K=1 plan, up to 12.9 GB per
+    checkpoint): each staged entry equals its source range, the device CRCs
+    of the CRC engine equal CRCs of the source ranges taken by a second
+    kernel pass, the staged total equals the planner workload, and an
+    unpack into the wiped ranges restores them bit-exactly (device-side
+    comparisons; sizes where a CPU oracle pass would take minutes)."""
+    import torch
+    from paper_2408_04307_b200 import configs, plan_adaptive
+    from paper_2408_04307_b200 import device as D
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.staging import DeviceTable, StagingLayout
+    w = configs.mixtral_8x7b()
+    layout = w.layout()
+    plan = plan_adaptive(layout, w.pec)
+    arena = StateArena(layout, [0], dev, w.expert_tensors)
+    lg = D.DEFAULT_CHUNK_LOG2
+    phases = range(plan.period) if engine == "bulk" else [0]
+    staging = None
+    for ph in phases:
+        st = StagingLayout.build(plan.assignments[ph][0], arena, 0)
+        assert st.payload_bytes == plan.workload_bytes[ph][0]
+        if staging is None or staging.numel() < st.nbytes:
+            staging = None
+            torch.cuda.empty_cache()
+            staging = torch.empty(st.nbytes + 256, dtype=torch.uint8, device=dev)
+        table, total = st.descriptors(arena.base_address, staging.data_ptr(), chunk_log2=lg)
+        dt = DeviceTable(table, total, dev, lg)
+        if engine == "bulk":
+            D.pack(dt.tensor, dt.n, dt.total_chunks, lg, D.MODE_BULK)
+        else:
+            chunk = torch.empty(D.CRC_UNITS_PER_CHUNK * total, dtype=torch.int32, device=dev)
+            ecrc = torch.empty(dt.n, dtype=torch.int32, device=dev)
+            D.pack_crc(dt.tensor, dt.n, dt.total_chunks, chunk, ecrc, lg)
+            # independent check: host SSE4.2 CRC-32C of the smallest, a middle and
+            # the largest entry (copied back), against the device CRCs
+            order = sorted(range(len(st.entries)), key=lambda i: st.entries[i].nbytes)
+            for i in {order[0], order[len(order) // 2], order[-1]}:
+                e = st.entries[i]
+                host = arena.buffer[e.src_offset:e.src_offset + e.nbytes].cpu().numpy()
+                assert D.crc32c(host) == int(ecrc[i].item()) & 0xFFFFFFFF, e.store_key
+        torch.cuda.synchronize()
+        for e in st.entries:
+            assert torch.equal(staging[e.stage_offset:e.stage_offset + e.nbytes],
+                               arena.buffer[e.src_offset:e.src_offset + e.nbytes]), (ph, e.store_key)
+        # restore direction: wipe the ranges, unpack, compare again
+        for e in st.entries:
+            arena.buffer[e.src_offset:e.src_offset + e.nbytes].zero_()
+        D.unpack(dt.tensor, dt.n, dt.total_chunks, lg, D.MODE_BULK)
+        torch.cuda.synchronize()
+        for e in st.entries:
+            assert torch.equal(staging[e.stage_offset:e.stage_offset + e.nbytes],
+                               arena.buffer[e.src_offset:e.src_offset + e.nbytes]), (ph, e.store_key)
+    del staging, arena
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
 def test_gpt350m_k_sweep_pack_bit_exact_on_device(dev, k):
     """K_pec sweep on GPT-MoE 350M-16E (dp=8 x ep=8, ranks 0..7 emulated):
