@@ -553,7 +553,7 @@ def run_b200(args):
         else:
             try:
                 eng.reserve(eng.staging.numel(), host_buffers=n_host)
-            except (RuntimeError, MemoryError) as exc:  # e.g. pinning refused
+            except (RuntimeError, MemoryError, OSError) as exc:  # e.g. pinning refused
                 pin_error = f"{type(exc).__name__}: {exc}"[:200]
         pin_s = time.perf_counter() - tpin
         if max_over_ranks(1.0 if pin_error else 0.0, world, dev) > 0:
