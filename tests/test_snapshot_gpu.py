@@ -322,6 +322,44 @@ def test_mixtral_rank_full_size_pack_unpack_bit_exact(dev, engine):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("strategy", ["baseline", "equal_full"])
+def test_full_checkpoints_without_pec_save_and_restore_every_unit(dev, tmp_path, strategy):
+    """pec=None: the reference's full-checkpoint strategies (plan_baseline /
+    plan_equal without K_pec, planner.py:322-334) -- every unit in every
+    version, the planner's per-rank workload staged, and a wiped state
+    restored bit-exactly from the newest version."""
+    import torch
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.restore import restore
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore
+    layout = make_layout(n_experts=4, dp=4, ep=2, gpus_per_node=2, epp=300_001, other=1000)
+    ranks = list(range(layout.n_ranks))
+    arena = StateArena(layout, ranks, dev)
+    store = DiskStore(tmp_path)
+    ck = PecCheckpointer(layout, arena, store, None, strategy, i_ckpt=2, ranks=ranks)
+    plan = ck.plan()
+    assert plan.period == 1
+    for it in range(1, 7):
+        _mutate(arena, it)
+        buf = ck.step(it)
+        if buf is not None:
+            ck.wait_pack()
+    ck.finish()
+    torch.cuda.synchronize()
+    good = arena.buffer.cpu().numpy().copy()
+    vs = store.complete_versions()
+    assert len(vs) == 3
+    units = {e.unit_key for e in store.meta(vs[-1]).entries.values()}
+    assert units == {u.key for u in layout.units if u.size_bytes > 0}
+    assert sum(ck.engine.stats["snap_bytes"][-1:]) == sum(plan.workload_bytes[0].values())
+    rp = ck.engine.resolve_recovery({1})     # node 1 lost: its units come from storage
+    arena.buffer.zero_()
+    restore(ck.engine, rp)
+    assert np.array_equal(arena.buffer.cpu().numpy(), good)
+    ck.close()
+
+
 @pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
 def test_gpt350m_k_sweep_pack_bit_exact_on_device(dev, k):
     """K_pec sweep on GPT-MoE 350M-16E (dp=8 x ep=8, ranks 0..7 emulated):
