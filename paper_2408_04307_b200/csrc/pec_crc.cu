@@ -10,19 +10,22 @@
 // CRC-32C is linear over GF(2): for the register form R (initial value 0,
 // no final inversion), R(A || B) = R(A) * x^(8|B|) mod P  ^  R(B), and the
 // standard CRC is crc(M) = ~(R(M) ^ ~0 * x^(8|M|) mod P).  So:
-//   pack_crc_kernel   each thread copies 128 contiguous bytes of a 32 KiB
-//                     chunk and folds them with a byte table kept in shared
-//                     memory once per lane (entry e of lane l at word
-//                     32e + l: every lookup of a warp hits 32 distinct
-//                     banks), then a warp shuffle tree and a cross-warp fold
-//                     combine the 256 partial registers with constant
-//                     shifts -> one register per chunk;
-//   crc_fold_kernel   one thread per chunk shifts its register by the bytes
-//                     that follow it in its entry and XORs it into the
-//                     entry's register (XOR is associative/commutative);
+//   pack_crc_kernel   one warp per 4 KiB unit: coalesced 16 B loads, stored
+//                     to staging and through a swizzled per-warp tile so each
+//                     lane then folds ITS contiguous 128 B in four 32-byte
+//                     chains with a byte table kept in shared memory once per
+//                     lane (entry e of lane l at word 32e + l: every lookup of
+//                     a warp hits 32 distinct banks); each lane shifts its
+//                     register to the unit end with its own constant (lane-
+//                     replicated 4-bit-window tables) and a 5-step XOR
+//                     butterfly gives the unit register;
+//   crc_fold_kernel   one thread per 32 KiB chunk joins its 8 unit registers,
+//                     shifts the result by the bytes that follow it in its
+//                     entry and XORs it into the entry's register;
 //   crc_final_kernel  applies the initial value / final inversion per entry.
 // Multiplication mod P (reflected, bit 31 = x^0) is the shift-and-add
-// schoolbook product; x^(2^k) are precomputed on the host.
+// schoolbook product or, for constants, 8 lookups of 4-bit-window tables;
+// x^(2^k) are precomputed on the host.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -112,39 +115,83 @@ __device__ __forceinline__ uint32_t mul_const(const uint32_t* nib, uint32_t b) {
 constexpr int kUnitLog2 = 12;
 constexpr int kUnitsPerChunk = 1 << (kCrcLg - kUnitLog2);
 
-__global__ void __launch_bounds__(kCrcThreads, 2)
+// Multipliers the pack kernel builds 4-bit-window tables for (128 words each):
+// [0] x^(8*32) joins a lane's 32-byte chains, [1] x^(8*S) joins its
+// sub-blocks (S = 4096 / kSub bytes), [2..6] x^(8*P*2^j) are the warp-tree
+// levels (P = 128 / kSub bytes per lane per sub-block).
+constexpr int kPackMuls = 7;
+constexpr int kPackMulWords = kPackMuls * 128;
+constexpr int kLaneTabWords = 8 * 16 * 32;  // per-lane x^(8*P*(31-l)) windows
+
+template <int kThreads, int kSub, bool kLaneMul>
+constexpr int pack_crc_smem() {
+  return (kTableWords + (kLaneMul ? 2 * 128 : kPackMulWords) + (kLaneMul ? kLaneTabWords : 0)) * 4 +
+         (kThreads / 32) * (4096 / kSub);
+}
+
+// kSub: the 4 KiB unit is transposed through a (4096 / kSub)-byte per-warp
+// tile in kSub rounds (smaller tiles: more CTAs per SM).  kLaneMul: a full
+// unit's lanes shift their registers to the unit end with per-lane constant
+// tables (lane l's window table at word 32 * (16 p + v) + l: conflict-free)
+// and a 5-step XOR butterfly, instead of the 5-level multiply tree.
+template <int kThreads, int kSub, int kMinBlocks, bool kLaneMul>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
                 const uint64_t* __restrict__ total_dev, CrcConsts k,
                 uint32_t* __restrict__ unit_raw) {
-  // dynamic smem: byte table | nibble tables | per-warp 4 KiB transpose tiles
+  constexpr int kVecSub = kVecPerThread / kSub;   // 16-byte vectors per lane per round
+  constexpr int kChains = 4 / kSub;               // 32-byte chains per round
+  constexpr int kPiece = kPerThread / kSub;       // bytes per lane per round
+  // dynamic smem: byte table | multiplier windows | lane windows | per-warp tiles
+  constexpr int kMuls = kLaneMul ? 2 : kPackMuls;  // tree levels only without lane tables
   extern __shared__ __align__(16) uint32_t table[];
   uint32_t* nib = table + kTableWords;
-  uint32_t* stage = table + kTableWords + kMulWords;
+  uint32_t* lanetab = nib + kMuls * 128;
+  uint32_t* stage = lanetab + (kLaneMul ? kLaneTabWords : 0);
+  __shared__ uint32_t mconst[kPackMuls];
+  __shared__ uint32_t lconst[32];
   if (total_dev != nullptr) {
     const uint64_t td = *total_dev;
     total = td < total ? td : total;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < kTableWords; idx += kCrcThreads) {
+  if (tid < kMuls) {
+    const uint64_t bytes = tid == 0 ? 32 : tid == 1 ? 4096 / kSub
+                                             : (uint64_t)kPiece << (tid - 2);
+    mconst[tid] = xpow_bytes(k.x2k, bytes);
+  } else if (kLaneMul && tid >= 64 && tid < 96) {
+    const int l = tid - 64;
+    lconst[l] = xpow_bytes(k.x2k, (uint64_t)kPiece * (31 - l));
+  }
+  for (int idx = tid; idx < kTableWords; idx += kThreads) {
     uint32_t c = (uint32_t)(idx >> 5);
 #pragma unroll
     for (int b = 0; b < 8; ++b) c = (c & 1u) ? (c >> 1) ^ kPoly : c >> 1;
     table[idx] = c;
   }
-  for (int idx = tid; idx < kMulWords; idx += kCrcThreads) {
+  __syncthreads();
+  for (int idx = tid; idx < kMuls * 128; idx += kThreads) {
     const int m = idx >> 7, p = (idx >> 4) & 7, v = idx & 15;
-    nib[idx] = gf2_mul(k.mul[m], (uint32_t)v << (4 * p));
+    nib[idx] = gf2_mul(mconst[m], (uint32_t)v << (4 * p));
+  }
+  if (kLaneMul) {
+    for (int idx = tid; idx < kLaneTabWords; idx += kThreads) {
+      const int l = idx & 31, pv = idx >> 5, p = pv >> 4, v = pv & 15;
+      lanetab[idx] = gf2_mul(lconst[l], (uint32_t)v << (4 * p));
+    }
   }
   __syncthreads();
   const uint32_t* tab = table + lane;
-  const uint32_t* s32 = nib;                 // x^(8*32)
-  const uint32_t* lvl = nib + 128;           // lane tree levels, 128 words each
-  int4* tile = reinterpret_cast<int4*>(stage) + warp * 256;
+  const uint32_t* n32 = nib;
+  const uint32_t* nsub = nib + 128;
+  const uint32_t* lvl = nib + 256;           // tree levels, 128 words each
+  const uint32_t* ltab = lanetab + lane;
+  int4* tile = reinterpret_cast<int4*>(stage) + warp * (256 / kSub);
 
   const uint64_t units = total * kUnitsPerChunk;
-  const uint64_t warps_total = (uint64_t)gridDim.x * (kCrcThreads / 32);
+  const uint64_t warps_total = (uint64_t)gridDim.x * (kThreads / 32);
   pecdev::DescCursor cur;
-  for (uint64_t u = (uint64_t)blockIdx.x * (kCrcThreads / 32) + warp; u < units;
+  for (uint64_t u = (uint64_t)blockIdx.x * (kThreads / 32) + warp; u < units;
        u += warps_total) {
     const uint64_t ch = u >> (kCrcLg - kUnitLog2);
     const int i = cur.find(d, n, ch);
@@ -165,42 +212,62 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
     uint32_t my_len;
     if (fast) {
       // coalesced 16 B units (lane + 32k) -> staging, and into a swizzled tile
-      // from which each lane reads back ITS contiguous 128 B conflict-free
-      // (16-byte slot of unit x: x ^ ((x >> 3) & 7)); four 32-byte CRC chains.
+      // from which each lane reads back ITS contiguous piece conflict-free
+      // (16-byte slot of unit x: x ^ ((x >> 3) & 7)); 32-byte CRC chains.
       const int4* vs = reinterpret_cast<const int4*>(s);
       int4* vt = reinterpret_cast<int4*>(t);
       int4 r[kVecPerThread];
 #pragma unroll
       for (int q = 0; q < kVecPerThread; ++q) r[q] = __ldg(vs + lane + 32 * q);
 #pragma unroll
-      for (int q = 0; q < kVecPerThread; ++q) {
-        __stcs(vt + lane + 32 * q, r[q]);
-        const int x = lane + 32 * q;
-        tile[x ^ ((x >> 3) & 7)] = r[q];
-      }
-      __syncwarp();
+      for (int q = 0; q < kVecPerThread; ++q) __stcs(vt + lane + 32 * q, r[q]);
 #pragma unroll
-      for (int j = 0; j < kVecPerThread; ++j) {
-        const int x = lane * kVecPerThread + j;
-        r[j] = tile[x ^ ((x >> 3) & 7)];
-      }
-      uint32_t q4[4] = {0u, 0u, 0u, 0u};
+      for (int sb = 0; sb < kSub; ++sb) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+        for (int q = 0; q < kVecSub; ++q) {
+          const int x = lane + 32 * q;
+          tile[x ^ ((x >> 3) & 7)] = r[sb * kVecSub + q];
+        }
+        __syncwarp();
+        int4 v4[kVecSub];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
+        for (int j = 0; j < kVecSub; ++j) {
+          const int x = lane * kVecSub + j;
+          v4[j] = tile[x ^ ((x >> 3) & 7)];
+        }
+        __syncwarp();  // the tile is rewritten next
+        uint32_t q4[kChains];
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            const int4 v = r[cc * 2 + h];
-            const uint32_t word = w == 0 ? (uint32_t)v.x : w == 1 ? (uint32_t)v.y
-                                : w == 2 ? (uint32_t)v.z : (uint32_t)v.w;
-            q4[cc] = fold_word(tab, q4[cc], word);
+        for (int cc = 0; cc < kChains; ++cc) q4[cc] = 0u;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+#pragma unroll
+            for (int cc = 0; cc < kChains; ++cc) {
+              const int4 v = v4[cc * 2 + h];
+              const uint32_t word = w == 0 ? (uint32_t)v.x : w == 1 ? (uint32_t)v.y
+                                  : w == 2 ? (uint32_t)v.z : (uint32_t)v.w;
+              q4[cc] = fold_word(tab, q4[cc], word);
+            }
           }
         }
+        uint32_t cs = q4[0];
+#pragma unroll
+        for (int cc = 1; cc < kChains; ++cc) cs = mul_const(n32, cs) ^ q4[cc];
+        c = sb == 0 ? cs : mul_const(nsub, c) ^ cs;
       }
-      __syncwarp();  // the tile is rewritten by this warp's next unit
-      c = mul_const(s32, mul_const(s32, mul_const(s32, q4[0]) ^ q4[1]) ^ q4[2]) ^ q4[3];
-      my_len = kPerThread;
+      my_len = kPiece;
+      if (kLaneMul) {
+        // shift to the unit end with this lane's constant, XOR over the warp
+        uint32_t x = 0;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) x ^= ltab[(p * 16 + ((c >> (4 * p)) & 15u)) << 5];
+#pragma unroll
+        for (int j = 16; j >= 1; j >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, j);
+        if (lane == 0) unit_raw[u] = x;
+        continue;
+      }
     } else {
       // partial or unaligned unit: bytes, 128 per lane
       const uint64_t lo = (uint64_t)lane * kPerThread;
@@ -212,7 +279,7 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
       }
       my_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
     }
-    // warp tree: lanes hold consecutive 128 B pieces; fold right neighbours in
+    // warp tree: lanes hold consecutive pieces; fold right neighbours in
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
       const uint32_t oc = __shfl_down_sync(0xffffffffu, c, 1 << j);
@@ -224,6 +291,29 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
     }
     if (lane == 0) unit_raw[u] = c;
   }
+}
+
+template <int kThreads, int kSub, int kMinBlocks, bool kLaneMul>
+int launch_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
+                    const uint64_t* total_chunks_dev, const CrcConsts& consts,
+                    uint32_t* chunk_crc, cudaStream_t st) {
+  auto kern = pack_crc_kernel<kThreads, kSub, kMinBlocks, kLaneMul>;
+  constexpr int smem = pack_crc_smem<kThreads, kSub, kLaneMul>();
+  static const int per_sm = [&] {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return 0;
+    int blocks = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kThreads, smem);
+    return blocks < 1 ? 1 : blocks;
+  }();
+  if (per_sm == 0) return PEC_E_CUDA;
+  uint64_t grid = (uint64_t)sm_count() * per_sm;
+  const uint64_t need = (total_chunks * kUnitsPerChunk + kThreads / 32 - 1) / (kThreads / 32);
+  if (grid > need) grid = need;
+  kern<<<(unsigned)grid, kThreads, smem, st>>>(descs, n, total_chunks, total_chunks_dev, consts,
+                                                   chunk_crc);
+  return PEC_OK;
 }
 
 // One thread per chunk: join the chunk's 8 unit registers (constant 4 KiB
@@ -307,22 +397,11 @@ int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
   if (cudaMemsetAsync(entry_crc, 0, sizeof(uint32_t) * (size_t)n, st) != cudaSuccess)
     return PEC_E_CUDA;
   if (total_chunks > 0) {
-    // launch geometry once per process (attribute/occupancy queries are not free)
-    static const int smem = (kTableWords + kMulWords) * (int)sizeof(uint32_t) + kCrcThreads * 128;
-    static const int per_sm = [] {
-      if (cudaFuncSetAttribute(pack_crc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               smem) != cudaSuccess)
-        return 0;
-      int blocks = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pack_crc_kernel, kCrcThreads, smem);
-      return blocks < 1 ? 1 : blocks;
-    }();
-    if (per_sm == 0) return PEC_E_CUDA;
-    uint64_t grid = (uint64_t)sm_count() * per_sm;
-    const uint64_t need = (total_chunks * kUnitsPerChunk + kCrcThreads / 32 - 1) / (kCrcThreads / 32);
-    if (grid > need) grid = need;
-    pack_crc_kernel<<<(unsigned)grid, kCrcThreads, smem, st>>>(descs, n, total_chunks,
-                                                                total_chunks_dev, consts, chunk_crc);
+    // measured on B200 (profiles/r1/crc_variants.txt): lane-constant shifts
+    // instead of the multiply tree, 4 KiB tiles, 2 CTAs x 8 warps per SM
+    const int rc = launch_pack_crc<256, 1, 3, true>(descs, n, total_chunks, total_chunks_dev,
+                                                     consts, chunk_crc, st);
+    if (rc != PEC_OK) return rc;
     uint64_t fold_grid = (total_chunks + 255) / 256;
     if (fold_grid > (uint64_t)sm_count() * 8) fold_grid = (uint64_t)sm_count() * 8;
     crc_fold_kernel<<<(unsigned)fold_grid, 256, 0, st>>>(descs, n, total_chunks, total_chunks_dev,
