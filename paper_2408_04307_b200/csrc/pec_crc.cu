@@ -47,15 +47,12 @@ constexpr int kPerThread = (1 << kCrcLg) / kCrcThreads;  // 128 contiguous bytes
 constexpr int kVecPerThread = kPerThread / 16;        // 8 x 16 B
 constexpr int kTableWords = 256 * 32;                 // lane-replicated byte table
 
-// Constant multipliers, applied through 4-bit windows: mul(a, b) =
+// Constant multipliers are applied through 4-bit windows: mul(a, b) =
 // XOR_p N_a[p][(b >> 4p) & 15] with N_a[p][v] = a * (v << 4p): 8 shared-memory
-// lookups instead of a 32-step schoolbook product.
-constexpr int kNumMul = 9;  // S32, lane levels 128..2048 B, warp levels 4..16 KiB
-constexpr int kMulWords = kNumMul * 8 * 16;
-
+// lookups instead of a 32-step schoolbook product (tables built per CTA).
 struct CrcConsts {
   uint32_t x2k[64];         // x^(2^k) mod P
-  uint32_t mul[kNumMul];    // x^(8*32), x^(8*128*2^j) j<5, x^(8*4096*2^j) j<3
+  uint32_t unit;            // x^(8 * 4096): one 4 KiB unit
 };
 
 __host__ __device__ __forceinline__ uint32_t gf2_mul(uint32_t a, uint32_t b) {
@@ -81,17 +78,6 @@ __device__ __forceinline__ uint32_t xpow_bytes(const uint32_t* x2k, uint64_t nby
 
 __device__ __forceinline__ uint32_t shift_bytes(const uint32_t* x2k, uint32_t r, uint64_t n) {
   return n ? gf2_mul(xpow_bytes(x2k, n), r) : r;
-}
-
-__device__ __forceinline__ int4 ld_cached(const int4* p) {
-  int4 r;
-  asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
-  asm volatile("st.global.cs.v4.s32 [%0], {%1, %2, %3, %4};"
-               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
 __device__ __forceinline__ uint32_t fold_word(const uint32_t* tab, uint32_t c, uint32_t w) {
@@ -316,25 +302,79 @@ int launch_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
   return PEC_OK;
 }
 
-// One thread per chunk: join the chunk's 8 unit registers (constant 4 KiB
-// shifts for full units), shift by the bytes that follow the chunk in its
-// entry and XOR into the entry register.
-__global__ void crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
-                                const uint64_t* __restrict__ total_dev, CrcConsts k,
-                                const uint32_t* __restrict__ unit_raw,
-                                uint32_t* __restrict__ entry_raw) {
+// Chunk registers -> entry accumulators.  Each thread takes a contiguous run
+// of chunks, joins every chunk's (up to 8) unit registers (constant 4 KiB
+// shifts through 4-bit-window tables) and Horner-accumulates consecutive
+// chunks of one entry (constant 32 KiB shift), so an entry receives one
+// atomic per thread run instead of one per chunk (2 GB entries have 64 Ki
+// chunks: same-address atomics would serialise).  A run is flushed shifted
+// by the whole chunks that follow it, x^(8 * 32 KiB * j), a product of up to
+// three 256-entry power tables built per CTA by doubling.  The entry's LAST
+// chunk keeps its register in its own first unit slot (only this thread
+// touches that chunk's slots); crc_final_kernel applies the shift by the
+// last chunk's length once per entry and joins it.
+__global__ void __launch_bounds__(256)
+crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
+                const uint64_t* __restrict__ total_dev, CrcConsts k,
+                uint32_t* __restrict__ unit_raw, uint32_t* __restrict__ entry_raw) {
   __shared__ uint32_t x2k[64];
-  if (threadIdx.x < 64) x2k[threadIdx.x] = k.x2k[threadIdx.x];
+  __shared__ uint32_t unib[128];        // windows of x^(8 * 4096)
+  __shared__ uint32_t cnib[128];        // windows of x^(8 * 32768)
+  __shared__ uint32_t pw[3][256];       // x^(8 * 32K * t * 256^r)
+  const int tid = threadIdx.x;
+  if (tid < 64) x2k[tid] = k.x2k[tid];
   __syncthreads();
+  if (tid < 128) {
+    const int p = (tid >> 4) & 7, v = tid & 15;
+    unib[tid] = gf2_mul(k.unit, (uint32_t)v << (4 * p));
+  } else if (tid < 131) {
+    const int r = tid - 128;
+    uint32_t b = xpow_bytes(x2k, (uint64_t)(1u << kCrcLg) << (8 * r));
+    pw[r][0] = 1u << 31;
+    for (int l = 0; l < 8; ++l) {  // pw[r][2^l] = base^(2^l)
+      pw[r][1 << l] = b;
+      b = gf2_mul(b, b);
+    }
+  }
+  __syncthreads();
+  if (tid < 128) {
+    const int p = (tid >> 4) & 7, v = tid & 15;
+    cnib[tid] = gf2_mul(pw[0][1], (uint32_t)v << (4 * p));
+  }
+  for (int l = 1; l < 8; ++l) {     // pw[t] = pw[t - 2^l] * pw[2^l] for 2^l < t < 2^(l+1)
+    const int span = (1 << l) - 1;
+    for (int idx = tid; idx < 3 * span; idx += blockDim.x) {
+      const int r = idx / span, t = (1 << l) + 1 + idx % span;
+      pw[r][t] = gf2_mul(pw[r][t - (1 << l)], pw[r][1 << l]);
+    }
+    __syncthreads();
+  }
   if (total_dev != nullptr) {
     const uint64_t td = *total_dev;
     total = td < total ? td : total;
   }
-  const uint32_t unit_shift = k.mul[6];  // x^(8 * 4096)
-  for (uint64_t ch = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < total;
-       ch += (uint64_t)gridDim.x * blockDim.x) {
-    const int i = find_desc(d, n, ch);
-    const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << kCrcLg;
+  const uint64_t threads = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t per = (total + threads - 1) / threads;
+  const uint64_t c0 = ((uint64_t)blockIdx.x * blockDim.x + tid) * per;
+  const uint64_t c1 = c0 + per < total ? c0 + per : total;
+  pecdev::DescCursor cur;
+  int run_entry = -1;
+  uint32_t run = 0;                 // Horner sum of the run's chunk registers
+  uint64_t run_end = 0;             // entry-relative index one past the run
+  uint64_t run_chunks = 0;          // chunks of the run's entry
+  auto flush = [&]() {
+    if (run_entry < 0) return;
+    const uint64_t j = run_chunks - 1 - run_end;  // whole chunks up to the last one
+    uint32_t p = pw[0][j & 255];
+    if ((j >> 8) & 255) p = gf2_mul(p, pw[1][(j >> 8) & 255]);
+    if (j >> 16) p = gf2_mul(p, pw[2][(j >> 16) & 255]);
+    atomicXor(&entry_raw[run_entry], gf2_mul(run, p));
+    run_entry = -1;
+  };
+  for (uint64_t ch = c0; ch < c1; ++ch) {
+    const int i = cur.find(d, n, ch);
+    const uint64_t kk = ch - __ldg(&d[i].first_chunk);
+    const uint64_t off = kk << kCrcLg;
     const uint64_t nb = __ldg(&d[i].nbytes);
     if (off >= nb) continue;
     const uint64_t end = off + (1ull << kCrcLg) < nb ? off + (1ull << kCrcLg) : nb;
@@ -343,18 +383,43 @@ __global__ void crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint
       const uint64_t uoff = off + ((uint64_t)w << kUnitLog2);
       if (uoff >= end) break;
       const uint64_t ulen = end - uoff < (1ull << kUnitLog2) ? end - uoff : (1ull << kUnitLog2);
-      acc = (ulen == (1ull << kUnitLog2) ? gf2_mul(unit_shift, acc) : shift_bytes(x2k, acc, ulen))
+      acc = (ulen == (1ull << kUnitLog2) ? mul_const(unib, acc) : shift_bytes(x2k, acc, ulen))
             ^ unit_raw[ch * kUnitsPerChunk + w];
     }
-    atomicXor(&entry_raw[i], shift_bytes(x2k, acc, nb - end));
+    const uint64_t chunks = (nb + (1ull << kCrcLg) - 1) >> kCrcLg;
+    if (run_entry >= 0 && i != run_entry) flush();
+    if (kk == chunks - 1) {
+      unit_raw[ch * kUnitsPerChunk] = acc;   // R(last chunk), joined in crc_final_kernel
+      flush();                               // this entry's run (if any) ends right before it
+      continue;
+    }
+    if (run_entry < 0) {
+      run_entry = i;
+      run = 0;
+      run_chunks = chunks;
+    }
+    run = mul_const(cnib, run) ^ acc;
+    run_end = kk + 1;
   }
+  flush();
 }
 
+// Per entry: R = A * x^(8 * len(last chunk)) ^ R(last chunk), then the
+// initial value / final inversion: crc = ~(R ^ ~0 * x^(8 * nbytes)).
 __global__ void crc_final_kernel(const pec_copy_desc* __restrict__ d, int n, CrcConsts k,
+                                 const uint32_t* __restrict__ unit_raw,
                                  uint32_t* __restrict__ entry) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint64_t nb = d[i].nbytes;
-    entry[i] = nb ? ~(entry[i] ^ shift_bytes(k.x2k, 0xFFFFFFFFu, nb)) : 0u;
+    if (nb == 0) {
+      entry[i] = 0u;
+      continue;
+    }
+    const uint64_t chunks = (nb + (1ull << kCrcLg) - 1) >> kCrcLg;
+    const uint64_t last_len = nb - ((chunks - 1) << kCrcLg);
+    const uint32_t r_last = unit_raw[(d[i].first_chunk + chunks - 1) * kUnitsPerChunk];
+    const uint32_t r = shift_bytes(k.x2k, entry[i], last_len) ^ r_last;
+    entry[i] = ~(r ^ shift_bytes(k.x2k, 0xFFFFFFFFu, nb));
   }
 }
 
@@ -375,9 +440,7 @@ CrcConsts make_consts() {
     }
     return acc;
   };
-  k.mul[0] = xpow(32);
-  for (int j = 0; j < 5; ++j) k.mul[1 + j] = xpow((uint64_t)kPerThread << j);
-  for (int j = 0; j < 3; ++j) k.mul[6 + j] = xpow((uint64_t)kPerThread * 32 << j);
+  k.unit = xpow(1u << kUnitLog2);
   return k;
 }
 
@@ -403,11 +466,11 @@ int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
                                                      consts, chunk_crc, st);
     if (rc != PEC_OK) return rc;
     uint64_t fold_grid = (total_chunks + 255) / 256;
-    if (fold_grid > (uint64_t)sm_count() * 8) fold_grid = (uint64_t)sm_count() * 8;
+    if (fold_grid > (uint64_t)sm_count()) fold_grid = (uint64_t)sm_count();  // tables per CTA
     crc_fold_kernel<<<(unsigned)fold_grid, 256, 0, st>>>(descs, n, total_chunks, total_chunks_dev,
                                                           consts, chunk_crc, entry_crc);
   }
-  crc_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(descs, n, consts, entry_crc);
+  crc_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(descs, n, consts, chunk_crc, entry_crc);
   return launch_status();
 }
 
