@@ -532,8 +532,8 @@ def run_b200(args):
     persist_info = None
     pin_s = 0.0
     if not (args.no_e2e and args.no_stall):
-        # pin the host snapshot buffers once, before any timing (cudaHostAlloc
-        # pins ~2 GB/s; a training job does this at start-up): 3 with a
+        # pin the host snapshot buffers once, before any timing (pinning runs
+        # at ~4-5 GB/s; a training job does this at start-up): 3 with a
         # persist tier, 2 without (buffers then recycle through RECOVERY)
         tpin = time.perf_counter()
         pin_error = None
@@ -545,9 +545,19 @@ def run_b200(args):
         if n_host < want:
             print(f"bench: host RAM fits {n_host} of {want} pinned snapshot buffers per rank",
                   file=sys.stderr)
-        if n_host < 2:
-            args.no_stall = True     # the loop cycles >= 2 buffers
-            args.e2e_steps = 1
+        # pinned buffers each leg cycles through (an unpinned one would be
+        # allocated inside a timed region): the stall loop needs RECOVERY +
+        # PERSISTING + SNAPSHOTTING with a persist tier (2 without); the e2e
+        # leg holds the persist tier, so its warm step plus every timed step
+        # need their own buffer with one (buffers recycle without)
+        if n_host < (3 if store is not None else 2):
+            args.no_stall = True
+        warm_e2e = n_host >= 2
+        if store is not None:
+            e2e_cap = n_host - 1 if warm_e2e else 1
+        else:
+            e2e_cap = 2 if warm_e2e else 1
+        args.e2e_steps = max(1, min(args.e2e_steps, e2e_cap))
         if n_host < 1:
             pin_error = "host RAM too small for one pinned snapshot buffer per local rank"
         else:
@@ -619,8 +629,9 @@ def run_b200(args):
 
         # one untimed step through the same calls (first-call host costs), then
         # its persist drains before the timed steps
-        e2e_step(e2e_steps, base_it - args.i_ckpt)
-        ck.finish()
+        if warm_e2e:
+            e2e_step(e2e_steps, base_it - args.i_ckpt)
+            ck.finish()
         h2d = d2h = 0
         n_persist0 = len(eng.stats["persist_s"])
         barrier(world)

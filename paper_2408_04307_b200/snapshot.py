@@ -894,7 +894,7 @@ class PecCheckpointer:
                 self._start_persist(p)
 
     def _start_persist(self, buf: Buffer) -> None:
-        if getattr(self, "_persist_held", False):
+        if getattr(self, "_persist_held", False) and self.engine.store is not None:
             return  # stays PERSISTING (queued) until hold_persist(False)
         if self.engine.store is None:
             # snapshot tier only (no persist tier configured): the buffer is
