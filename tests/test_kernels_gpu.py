@@ -293,6 +293,40 @@ def test_pack_crc_copies_and_checksums_every_entry(dev, congruent):
         assert int(c) == O.crc32c(host[s:s + n]), (s, n)
 
 
+def test_pack_crc_very_long_entries_use_every_power_table(dev):
+    """Entries long enough that the chunk shifts need all three power tables
+    (> 65536 whole 32 KiB chunks after a chunk: a 2 GiB+ entry), plus entries
+    of exactly k x 32 KiB, k x 32 KiB + 1 and 257 chunks: device CRCs equal the
+    host SSE4.2 CRC-32C of the same bytes and the copies are exact."""
+    import torch
+    from paper_2408_04307_b200 import device as D
+    lens = [(1 << 31) + 12345, 32768 * 3, 32768 * 3 + 1, 32768 * 257 - 7, 1]
+    size = sum(lens) + 256 * len(lens)
+    state = torch.empty(size, dtype=torch.uint8, device=dev)
+    state.view(torch.int32)[: size // 4].random_()
+    staging = torch.empty(size + 256, dtype=torch.uint8, device=dev)
+    table = np.zeros(len(lens), dtype=D.DESC_DTYPE)
+    pos = 0
+    for i, n in enumerate(lens):
+        table[i] = (state.data_ptr() + pos, staging.data_ptr() + pos + 128, n, 0)
+        pos += n + 256
+    total = D.plan_chunks(table, 15)
+    dt = torch.from_numpy(table.view(np.uint8).copy()).view(torch.int64).to(dev)
+    chunk = torch.empty(D.CRC_UNITS_PER_CHUNK * total, dtype=torch.int32, device=dev)
+    entry = torch.empty(len(lens), dtype=torch.int32, device=dev)
+    D.pack_crc(dt, len(lens), total, chunk, entry, 15)
+    torch.cuda.synchronize()
+    got = entry.cpu().numpy().view(np.uint32)
+    pos = 0
+    for i, n in enumerate(lens):
+        src = state[pos:pos + n]
+        assert torch.equal(staging[pos + 128:pos + 128 + n], src), n
+        assert int(got[i]) == D.crc32c(src.cpu().numpy()), n
+        pos += n + 256
+    del state, staging, chunk
+    torch.cuda.empty_cache()
+
+
 def test_c_abi_device_entry_points_from_plain_c(dev, tmp_path):
     """pack / unpack / sequential selection / histogram called from a plain C
     program through include/pec.h (tests/c/abi_check.c, CUDA runtime)."""
