@@ -866,6 +866,9 @@ class PecCheckpointer:
             at_r = self._cum_at.get(r, zero) if r else zero
             mask = restored == r
             unsaved[mask] = (base - at_r)[mask]
+        # a checkpoint taken before the counters were attached has no
+        # snapshot: never let a missing one turn into negative counts
+        unsaved.clamp_(min=0)
         self.counters.reset_to(unsaved, unsaved)
         self._replay_offset = self.counters.delivered - base
         self._cum_at = {k: v for k, v in self._cum_at.items() if k <= restart}
