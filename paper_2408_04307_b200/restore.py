@@ -166,38 +166,56 @@ def _pieces(engine, plan: RecoveryPlan, wanted, slot_bytes: int):
     return pieces, initial, peers
 
 
-_READ_STEP = 4 << 20  # CRC each 4 MiB right after reading it, while cache-hot
+_READ_STEP = 4 << 20   # CRC each 4 MiB right after reading it, while cache-hot
+_SUB_READ = 8 << 20    # file pieces are read as independent sub-ranges of this size
 
 
-def _read_piece_raw(item) -> None:
-    """Read a file piece into the pinned slot (CRC verified on the GPU)."""
-    p, off, host = item
-    view = memoryview(host.numpy()).cast("B")[off:off + p.nbytes]
-    with open(p.path, "rb", buffering=0) as f:
-        f.seek(p.file_off)
-        got = 0
-        while got < p.nbytes:
-            n = f.readinto(view[got:])
-            if not n:
-                raise ChecksumMismatchError(p.entry, "short read")
-            got += n
+def _sub_jobs(files):
+    """Split file pieces [(piece, slot_off, host)] into <= 8 MiB sub-reads so
+    the pool's threads share one large entry instead of one thread per
+    entry."""
+    jobs = []
+    for k, (p, off, host) in enumerate(files):
+        for lo in range(0, p.nbytes, _SUB_READ):
+            jobs.append((k, p.path, p.file_off + lo, host, off + lo, min(_SUB_READ, p.nbytes - lo),
+                         p.entry))
+    return jobs
 
 
-def _read_piece(item) -> int:
-    p, off, host = item
-    view = memoryview(host.numpy()).cast("B")[off:off + p.nbytes]
+def _read_sub(job, want_crc: bool):
+    """pread one sub-range into the pinned slot; its CRC-32C if asked (4 MiB
+    steps, cache-hot)."""
+    _, path, file_off, host, slot_off, n, entry = job
+    view = memoryview(host.numpy()).cast("B")[slot_off:slot_off + n]
     crc = 0
-    with open(p.path, "rb", buffering=0) as f:
-        f.seek(p.file_off)
+    fd = os.open(path, os.O_RDONLY)
+    try:
         got = 0
-        while got < p.nbytes:
-            want = min(_READ_STEP, p.nbytes - got)
-            n = f.readinto(view[got:got + want])
-            if not n:
-                raise ChecksumMismatchError(p.entry, "short read")
-            crc = crc32c(view[got:got + n], crc)
-            got += n
+        while got < n:
+            want = min(_READ_STEP, n - got)
+            k = os.preadv(fd, [view[got:got + want]], file_off + got)
+            if not k:
+                raise ChecksumMismatchError(entry, "short read")
+            if want_crc:
+                crc = crc32c(view[got:got + k], crc)
+            got += k
+    finally:
+        os.close(fd)
     return crc
+
+
+def _read_files(pool, files, want_crc: bool):
+    """Read every file piece of a batch with all pool threads; per-piece
+    CRC-32Cs (sub-range CRCs combined in order) when ``want_crc``."""
+    jobs = _sub_jobs(files)
+    crcs = list(pool.map(lambda j: _read_sub(j, want_crc), jobs))
+    if not want_crc:
+        return None
+    out = [None] * len(files)
+    for j, c in zip(jobs, crcs):
+        k, n = j[0], j[5]
+        out[k] = c if out[k] is None else D.crc32c_combine(out[k], c, n)
+    return [0 if c is None else c for c in out]
 
 
 def _chain(running: Dict[str, int], p: "_Piece", crc: int) -> None:
@@ -271,11 +289,7 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
                 ring.free[slot].synchronize()   # slot's previous batch fully consumed
             hslot, dslot = ring.host[slot], ring.dev[slot]
             files = [(p, off, hslot) for p, off in batch if p.kind == "file"]
-            if verify == "device":
-                list(pool.map(_read_piece_raw, files))
-                crcs = None
-            else:
-                crcs = list(pool.map(_read_piece, files))
+            crcs = _read_files(pool, files, want_crc=verify == "host")
             for p, off in batch:
                 if p.kind == "bytes":
                     hslot.numpy()[off:off + p.nbytes] = np.frombuffer(
