@@ -96,7 +96,7 @@ int pec_select_load_aware(int64_t* counters, int L, int E, int K,
  * descs: DEVICE table of n copies (src = state, dst = staging), chunk
  * prefix filled by pec_plan_chunks with the same chunk_log2 (12..24).
  * mode: 0 = auto (TMA bulk), 1 = vectorised LDG/STG.128 engine, 2 = TMA bulk
- * (cp.async.bulk) engine; 10-20 = bulk ring/occupancy/narrow-grid variants (benchmarking).  Ranges may be byte-granular; the fast path needs
+ * (cp.async.bulk) engine; 10-23 = bulk ring/occupancy/narrow-grid variants (benchmarking).  Ranges may be byte-granular; the fast path needs
  * src == dst (mod 16), which the staging layout guarantees. */
 int pec_pack(const pec_copy_desc* descs, int n, uint64_t total_chunks,
              int chunk_log2, int mode, void* stream);

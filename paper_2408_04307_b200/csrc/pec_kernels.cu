@@ -648,12 +648,12 @@ int launch_vec(const pec_copy_desc* descs, int n, uint64_t total, const uint64_t
 }
 
 // mode 1: vector engine; 2: TMA bulk engine (the default); 10-16: bulk-engine
-// ring/occupancy variants, 17-20: on 1/2 .. 1/8 of the SMs, kept for
+// ring/occupancy variants, 17-20: on 1/2 .. 1/8 of the SMs, 21-23: two CTAs per SM, kept for
 // benchmarking (tools/pack_variants.py, tools/overlap_probe.py).
 int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, const uint64_t* total_dev,
                 int lg, int mode, void* stream) {
   if (n < 0 || lg < 12 || lg > 24) return PEC_E_INVAL;
-  const bool known = (mode >= 0 && mode <= 2) || (mode >= 10 && mode <= 20);
+  const bool known = (mode >= 0 && mode <= 2) || (mode >= 10 && mode <= 23);
   if (!known) return PEC_E_INVAL;
   if (total == 0 || n == 0) return PEC_OK;
   if (descs == nullptr) return PEC_E_INVAL;
@@ -672,6 +672,10 @@ int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, const uint64_
     case 18: return launch_bulk<3, 15, true, 1, 4>(descs, n, total, total_dev, lg, st);
     case 19: return launch_bulk<6, 15, true, 1, 4>(descs, n, total, total_dev, lg, st);
     case 20: return launch_bulk<6, 15, true, 1, 8>(descs, n, total, total_dev, lg, st);
+    // two CTAs (two independent TMA rings) per SM
+    case 21: return launch_bulk<3, 15, true, 2>(descs, n, total, total_dev, lg, st);
+    case 22: return launch_bulk<2, 15, true, 2>(descs, n, total, total_dev, lg, st);
+    case 23: return launch_bulk<3, 14, true, 2>(descs, n, total, total_dev, lg, st);
     // default (measured best on B200, tools/pack_variants.py): one CTA per
     // SM, 3 x 32 KiB stages (two loads in flight while one stage drains),
     // L2 evict_first on both directions (streamed once; keeps L2 for the
