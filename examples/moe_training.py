@@ -56,10 +56,13 @@ def build(dev, seed: int = 0):
             n1 = d * ffn
             params[f"x{layer}.{e}.w1"] = (wv["w1"], ov["exp_avg"][:n1], ov["exp_avg_sq"][:n1])
             params[f"x{layer}.{e}.w2"] = (wv["w2"], ov["exp_avg"][n1:], ov["exp_avg_sq"][n1:])
-    # sane initial optimizer state (the seeded fill is synthetic): zeros
-    for _, (p, mm, vv) in params.items():
-        mm.zero_()
-        vv.zero_()
+    # the ZeRO flat partition is an opaque seeded blob: start its Adam
+    # moments at zero.  Expert moments keep their seeded initial images
+    # (exp_avg ~ N(0, 1e-3), exp_avg_sq = |N(0, 1e-6)|: valid Adam state), so
+    # the "initial" recovery source (arena.fill_unit) reproduces exactly the
+    # state an expert that was never saved started from.
+    flat_m.zero_()
+    flat_v.zero_()
     return w, layout, arena, params, dict(d=d, ffn=ffn, L=L, E=E, V=V, top_k=m.top_k)
 
 
@@ -123,9 +126,14 @@ def adam_step(params, step: int, lr=3e-3, b1=0.9, b2=0.999, eps=1e-8):
 
 
 def train(iters: int = 30, i_ckpt: int = 5, store_root=None, seed: int = 0, tokens: int = 512,
-          on_checkpoint=None):
+          on_checkpoint=None, fault_at: int = 0):
     """Returns (checkpointer, arena, losses, params).  ``on_checkpoint(buf)``
-    runs after each snapshot is started (state = the snapshotted state)."""
+    runs after each snapshot is started (state = the snapshotted state).
+    ``fault_at`` > 0 wipes the GPU state at that iteration (a lost node) and
+    recovers with `PecCheckpointer.recover`: partial-expert restore from host
+    memory / storage / initial images, load-aware counters reset, training
+    resumes at the restart iteration (batches are a function of the
+    iteration, so replayed iterations see the same data)."""
     import torch
     from paper_2408_04307_b200 import PecConfig
     from paper_2408_04307_b200.counting import DeviceTokenCounters
@@ -145,9 +153,11 @@ def train(iters: int = 30, i_ckpt: int = 5, store_root=None, seed: int = 0, toke
     pec = PecConfig(k_pec=2, selection="load_aware", k_snapshot=2, k_persist=1)
     ck = PecCheckpointer(layout, arena, store, pec, "equal_pec", i_ckpt=i_ckpt, counters=counters)
     ck.engine.reserve(ck.max_snapshot_bytes())
-    g = torch.Generator(device=dev).manual_seed(seed)
+    g = torch.Generator(device=dev)
     losses = []
-    for it in range(1, iters + 1):
+    it = 1
+    while it <= iters:
+        g.manual_seed(seed * 100003 + it)
         tok = torch.randint(0, shp["V"], (tokens,), device=dev, generator=g)
         tgt = tok                      # a learnable toy objective (reproduce the token)
         loss, ids = forward(params, shp, tok, tgt)
@@ -158,6 +168,16 @@ def train(iters: int = 30, i_ckpt: int = 5, store_root=None, seed: int = 0, toke
         if buf is not None and on_checkpoint is not None:
             on_checkpoint(buf)
         losses.append(float(loss.detach()))
+        if it == fault_at:
+            fault_at = 0               # one fault
+            ck.finish()                # (in-flight persists land or are discarded)
+            arena.buffer.zero_()       # the GPU state is gone
+            out = ck.recover({0}, it)  # node 0 lost: host snapshot copies too
+            for p, _, _ in params.values():
+                p.grad = None
+            it = out.restart_iteration + 1
+            continue
+        it += 1
     ck.finish()
     return ck, arena, losses, params
 
@@ -166,8 +186,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--store", default=None)
+    ap.add_argument("--fault-at", type=int, default=0)
     args = ap.parse_args()
-    ck, arena, losses, _ = train(args.iters, store_root=args.store)
+    ck, arena, losses, _ = train(args.iters, store_root=args.store, fault_at=args.fault_at)
     print(f"loss {losses[0]:.3f} -> {losses[-1]:.3f}; versions {ck.engine.store.complete_versions()}")
     ck.close()
 

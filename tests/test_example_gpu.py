@@ -62,3 +62,21 @@ def test_moe_training_loop_checkpoints_and_restores(dev, tmp_path):
                          torch.roll(tok, -1))
     assert torch.isfinite(loss)
     ck.close()
+
+
+def test_moe_training_loop_survives_a_node_fault(dev, tmp_path):
+    """The same loop with the GPU state wiped at iteration 10 (node 0 lost,
+    so only storage and initial images remain): PecCheckpointer.recover
+    restores it, training replays from the restart iteration and keeps
+    learning; the persisted versions stay loadable."""
+    import moe_training as ex
+    ck, arena, losses, params = ex.train(iters=16, i_ckpt=4, store_root=str(tmp_path),
+                                         tokens=256, fault_at=10)
+    assert all(np.isfinite(losses))
+    assert len(losses) == 16 + (10 - 8)      # iterations 9..10 replayed after restart 8
+    assert losses[-1] < losses[0]
+    versions = ck.engine.store.complete_versions()
+    assert len(versions) >= 4
+    for v in versions:
+        ck.engine.store.load_checkpoint(v)   # CRC-verified
+    ck.close()
