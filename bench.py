@@ -725,6 +725,9 @@ def run_b200(args):
             hl = line["host_link"]
             hl["frac"] = round(hl["achieved"] / link_alone, 4)
             hl["frac_of_concurrent"] = round(hl["achieved"] / link_conc, 4)
+            # e2e is bounded by the host link every GPU drains through at once
+            e2e["per_gpu"] = round(e2e["value"] / world, 3)
+            e2e["frac_of_host_link"] = round(e2e["per_gpu"] / link_conc, 4)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
