@@ -3,7 +3,6 @@
 line with the driver's keys, and the host-buffer budget helper."""
 
 import json
-import os
 import subprocess
 import sys
 from pathlib import Path

@@ -5,11 +5,9 @@ import json
 import os
 import socket
 import sys
-import tempfile
 from pathlib import Path
 
 import numpy as np
-import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
 

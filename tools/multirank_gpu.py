@@ -17,7 +17,6 @@ point).  Prints one JSON line per rank; exits non-zero on any mismatch.
 import json
 import os
 import sys
-import tempfile
 import time
 from pathlib import Path
 

@@ -1,5 +1,5 @@
 """Probe the GPU box: host RAM, cores, NUMA, disk, pinned D2H/H2D bandwidth."""
-import os, subprocess, time, json, shutil
+import os, subprocess, time, json
 import torch
 
 def sh(c):

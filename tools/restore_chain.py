@@ -18,7 +18,6 @@ GB/s.  Prints one JSON document.
 """
 
 import json
-import os
 import shutil
 import sys
 import time
