@@ -440,7 +440,8 @@ def run_b200(args):
     if persist != "none":
         base = "/dev/shm" if persist == "shm" else tempfile.gettempdir()
         store_root = tempfile.mkdtemp(prefix="pec_bench_", dir=base)
-        store = DiskStore(store_root, io_threads=8, direct_io=args.direct_io)
+        store = DiskStore(store_root, io_threads=len(os.sched_getaffinity(0)),
+                          direct_io=args.direct_io)
     control = None
     if world > 1 and store is not None:
         import torch.distributed as dist
