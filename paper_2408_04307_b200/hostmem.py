@@ -1,4 +1,4 @@
-"""Pinned host snapshot buffers: process-private and node-shared.
+"""Node-shared pinned host snapshot buffers.
 
 The two-level design keeps each completed snapshot in CPU memory so that the
 surviving nodes' copies can serve recovery (engine.py:214-229; paper §4.2).
@@ -25,45 +25,6 @@ def _register(array: np.ndarray) -> None:
     rc = torch.cuda.cudart().cudaHostRegister(array.ctypes.data, array.nbytes, 0)
     if int(rc) != 0:
         raise RuntimeError(f"cudaHostRegister({array.nbytes} B) failed: {rc}")
-
-
-class PinnedHostBuffer:
-    """A process-private pinned host buffer: anonymous memory advised for
-    transparent huge pages, faulted in, then pinned with `cudaHostRegister`.
-    Same D2H bandwidth as `cudaHostAlloc` (57.1 GB/s on the B200 boxes) but
-    ~3x faster to set up (12 GiB: 2.7 s vs 8.6 s,
-    `profiles/r1/d2h_hugepage_probe.json`) -- pinning tens of GB of snapshot
-    buffers is start-up time of every rank."""
-
-    def __init__(self, nbytes: int):
-        import torch
-        self.nbytes = nbytes
-        self.mm = mmap.mmap(-1, nbytes, mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
-        try:
-            self.mm.madvise(mmap.MADV_HUGEPAGE)
-        except (AttributeError, OSError):
-            pass  # no THP on this kernel: 4 KiB pages, still correct
-        self.array = np.frombuffer(self.mm, dtype=np.uint8)
-        self.array[::4096] = 0  # fault every page in before pinning
-        _register(self.array)
-        self.registered = True
-        self.tensor = torch.from_numpy(self.array)
-
-    def close(self) -> None:
-        import torch
-        if self.registered:
-            torch.cuda.cudart().cudaHostUnregister(self.array.ctypes.data)
-            self.registered = False
-        self.tensor = None
-        self.array = None
-        try:
-            self.mm.close()
-        except BufferError:
-            pass  # a view is still alive; the mapping goes with it
-
-
-def buffer_name(prefix: str, rank: int, buffer_id: int) -> str:
-    return f"{prefix}.r{rank:04d}.b{buffer_id}"
 
 
 class SharedHostBuffer:

@@ -101,7 +101,6 @@ class DeviceCheckpointEngine(CheckpointEngine):
         super().__init__(layout, store, n_buffers)
         self.shared_prefix = shared_host_prefix
         self._shared: Dict[int, object] = {}
-        self._private: Dict[int, object] = {}   # buffer_id -> PinnedHostBuffer
         self.arena = arena
         self.device = arena.device
         self.ranks = tuple(ranks) if ranks is not None else arena.ranks
@@ -140,14 +139,12 @@ class DeviceCheckpointEngine(CheckpointEngine):
         h = self.host[buffer_id]
         if h is None or h.numel() < nbytes:
             if self.shared_prefix is None:
-                from .hostmem import PinnedHostBuffer
-                old = self._private.pop(buffer_id, None)
-                self.host[buffer_id] = None
-                if old is not None:
-                    old.close()
-                pb = PinnedHostBuffer(max(nbytes, 256))
-                self._private[buffer_id] = pb
-                self.host[buffer_id] = pb.tensor
+                # cudaHostAlloc through torch's pinned allocator: lifetime tied
+                # to the tensor (an anonymous THP mapping + cudaHostRegister
+                # sets up 3x faster, profiles/r1/d2h_hugepage_probe.json, but
+                # its registration outlives nothing safely on its own)
+                self.host[buffer_id] = torch.empty(max(nbytes, 256), dtype=torch.uint8,
+                                                   pin_memory=True)
             else:
                 from .hostmem import SharedHostBuffer, buffer_name
                 if len(self.ranks) != 1:
@@ -611,10 +608,6 @@ class DeviceCheckpointEngine(CheckpointEngine):
 
     def close(self) -> None:
         self._persist_pool.shutdown(wait=True)
-        for bid, pb in list(self._private.items()):
-            self.host[bid] = None
-            pb.close()
-        self._private.clear()
         for bid, shb in list(self._shared.items()):
             self._retract_meta(bid)
             self.host[bid] = None

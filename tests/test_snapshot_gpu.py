@@ -356,7 +356,14 @@ def test_full_checkpoints_without_pec_save_and_restore_every_unit(dev, tmp_path,
     rp = ck.engine.resolve_recovery({1})     # node 1 lost: its units come from storage
     arena.buffer.zero_()
     restore(ck.engine, rp)
-    assert np.array_equal(arena.buffer.cpu().numpy(), good)
+    now = arena.buffer.cpu().numpy()
+    bad = []
+    for key, s in arena.slots.items():
+        if not np.array_equal(now[s.offset:s.offset + s.size], good[s.offset:s.offset + s.size]):
+            d = rp.decisions[key]
+            diff = np.nonzero(now[s.offset:s.offset + s.size] != good[s.offset:s.offset + s.size])[0]
+            bad.append((key, d.source, d.node, d.version, int(diff[0]), len(diff), s.size))
+    assert not bad, bad
     ck.close()
 
 

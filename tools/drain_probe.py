@@ -1,8 +1,7 @@
 """Drain probe (measurement tool): staging -> pinned host copy GB/s for the
-bench's 12.62 GB Mixtral snapshot size vs a 1 GiB copy, into the engine's
-host-buffer flavour (THP + cudaHostRegister) and into cudaHostAlloc memory,
-single copy vs 1 GiB / 256 MiB chunks on one stream vs two streams.  Best of
-3 each.  Prints one JSON document."""
+bench's 12.62 GB Mixtral snapshot size vs a 1 GiB copy into pinned
+(cudaHostAlloc) memory, single copy vs 1 GiB / 256 MiB chunks on one stream
+vs two streams.  Best of 3 each.  Prints one JSON document."""
 import json
 import sys
 import time
@@ -13,13 +12,11 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 def main():
     import torch
-    from paper_2408_04307_b200.hostmem import PinnedHostBuffer
     dev = torch.device("cuda", 0)
     n = 12_620_806_144
     staging = torch.empty(n, dtype=torch.uint8, device=dev)
     staging.view(torch.int32)[: n // 4].random_()
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-    thp = PinnedHostBuffer(n)
     cha = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     out = {}
 
@@ -33,7 +30,7 @@ def main():
             b = min(b, time.perf_counter() - t)
         return round(nbytes / b / 1e9, 2)
 
-    for name, host in (("thp_register", thp.tensor), ("cudaHostAlloc", cha)):
+    for name, host in (("cudaHostAlloc", cha),):
         host[:n].copy_(staging)  # first touch
         res = {}
         res["1GiB"] = best(lambda: host[: 1 << 30].copy_(staging[: 1 << 30], non_blocking=True),
@@ -54,7 +51,6 @@ def main():
                 host[h:].copy_(staging[h:], non_blocking=True)
         res["two_streams"] = best(two, n)
         out[name] = res
-    thp.close()
     print(json.dumps(out, indent=1), flush=True)
 
 
