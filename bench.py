@@ -719,7 +719,11 @@ def run_b200(args):
             "stall": stall,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": (2 if plan is not None else 5) * args.steps,
+            # our kernels per timed step: selection (1 sequential; hist + 2
+            # selects + plan expansion load-aware) + the pack (1 launch; the
+            # CRC engine adds its chunk fold and final kernels)
+            "gpu_launches": ((1 if plan is not None else 4) +
+                             (3 if args.engine == "crc" else 1)) * args.steps,
             "fill_s": round(t_fill, 2),
         }
         if line["host_link"]:
