@@ -139,10 +139,10 @@ class DeviceCheckpointEngine(CheckpointEngine):
         h = self.host[buffer_id]
         if h is None or h.numel() < nbytes:
             if self.shared_prefix is None:
-                # cudaHostAlloc through torch's pinned allocator: lifetime tied
-                # to the tensor (an anonymous THP mapping + cudaHostRegister
-                # sets up 3x faster, profiles/r1/d2h_hugepage_probe.json, but
-                # its registration outlives nothing safely on its own)
+                # cudaHostAlloc through torch's pinned allocator (pinning
+                # lifetime tied to the tensor).  An anonymous THP mapping +
+                # cudaHostRegister sets up 3x faster but was withdrawn, see
+                # DESIGN.md section 3.
                 self.host[buffer_id] = torch.empty(max(nbytes, 256), dtype=torch.uint8,
                                                    pin_memory=True)
             else:
