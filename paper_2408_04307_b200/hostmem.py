@@ -20,11 +20,8 @@ import numpy as np
 SHM_DIR = "/dev/shm"
 
 
-def _register(array: np.ndarray) -> None:
-    import torch
-    rc = torch.cuda.cudart().cudaHostRegister(array.ctypes.data, array.nbytes, 0)
-    if int(rc) != 0:
-        raise RuntimeError(f"cudaHostRegister({array.nbytes} B) failed: {rc}")
+def buffer_name(prefix: str, rank: int, buffer_id: int) -> str:
+    return f"{prefix}.r{rank:04d}.b{buffer_id}"
 
 
 class SharedHostBuffer:

@@ -367,6 +367,55 @@ def test_full_checkpoints_without_pec_save_and_restore_every_unit(dev, tmp_path,
     ck.close()
 
 
+def test_memory_restore_from_a_peer_engines_node_shared_buffer(dev, tmp_path):
+    """Two engines in one process stand in for two rank processes of one
+    node (shared_host_prefix: /dev/shm buffers registered with CUDA).  After
+    a checkpoint on both, rank 0's wiped state is restored from memory, with
+    the ranges that rank 1 snapshotted read out of rank 1's shared buffer
+    (`peer_buffer`), bit-identically."""
+    import os
+    import uuid
+    import torch
+    from paper_2408_04307_b200 import PecConfig
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.restore import restore
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import MemoryStore
+    layout = make_layout(n_experts=4, dp=2, ep=2, gpus_per_node=2, epp=20_001, other=100)
+    prefix = f"pec_gpu_{uuid.uuid4().hex[:8]}"
+    arenas = [StateArena(layout, [r], dev) for r in (0, 1)]
+    store = MemoryStore()
+    cks = [PecCheckpointer(layout, arenas[r], store, PecConfig(k_pec=2), "equal_pec", i_ckpt=1,
+                           ranks=[r], shared_host_prefix=prefix, async_persist=False)
+           for r in (0, 1)]
+    try:
+        _mutate(arenas[0], 1)
+        _mutate(arenas[1], 1)
+        for ck in cks:
+            ck.step(1)
+        for ck in cks:
+            ck.finish()
+        torch.cuda.synchronize()
+        good = arenas[0].buffer.cpu().numpy().copy()
+        plan = cks[0].engine.resolve_recovery(set())
+        mem = [k for k, d in plan.decisions.items() if d.source == "memory" and arenas[0].has(k)]
+        assert mem
+        # ranges of units resident on rank 0 that only rank 1 snapshotted
+        peer_keys = {a.key for a in cks[1].engine.buffers.buffers[0].content.get(1, ())}
+        assert peer_keys & set(mem)
+        arenas[0].buffer.zero_()
+        restore(cks[0].engine, plan, keys=mem)
+        now = arenas[0].buffer.cpu().numpy()
+        for k in mem:
+            s = arenas[0].slot(k)
+            assert np.array_equal(now[s.offset:s.offset + s.size],
+                                  good[s.offset:s.offset + s.size]), k
+    finally:
+        for ck in cks:
+            ck.close()
+    assert not [f for f in os.listdir("/dev/shm") if f.startswith(prefix)]
+
+
 @pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
 def test_gpt350m_k_sweep_pack_bit_exact_on_device(dev, k):
     """K_pec sweep on GPT-MoE 350M-16E (dp=8 x ep=8, ranks 0..7 emulated):

@@ -244,7 +244,8 @@ def test_fig7_two_level_recovery():
 
 def test_shared_host_buffer_visible_to_a_peer_mapping():
     import uuid
-    from paper_2408_04307_b200.hostmem import SharedHostBuffer
+    from paper_2408_04307_b200.hostmem import SharedHostBuffer, buffer_name
+    assert buffer_name("pfx", 3, 1) == "pfx.r0003.b1"   # peers derive each other's names
     name = f"pec_test_{uuid.uuid4().hex}"
     owner = SharedHostBuffer(name, 1 << 16, create=True, register=False)
     owner.array[100:110] = np.arange(10, dtype=np.uint8)
