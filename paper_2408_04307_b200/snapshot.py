@@ -210,8 +210,10 @@ class DeviceCheckpointEngine(CheckpointEngine):
             shb = SharedHostBuffer(buffer_name(self.shared_prefix, rank, bid), create=False,
                                    register=False)
             st = StagingLayout.build(buf.content.get(rank, ()), PeerSlots(self.layout, rank), rank)
-            if st.nbytes != meta["nbytes"]:
-                raise RuntimeError(f"peer rank {rank} v{version}: layout size mismatch")
+            # the owner publishes its region size, rounded up to 256 B
+            if (st.nbytes + 255) // 256 * 256 != meta["nbytes"]:
+                raise RuntimeError(f"peer rank {rank} v{version}: layout size mismatch "
+                                   f"({st.nbytes} B vs {meta['nbytes']} B published)")
             return shb, st
         return None
 

@@ -384,8 +384,8 @@ def test_memory_restore_from_a_peer_engines_node_shared_buffer(dev, tmp_path):
     layout = make_layout(n_experts=4, dp=2, ep=2, gpus_per_node=2, epp=20_001, other=100)
     prefix = f"pec_gpu_{uuid.uuid4().hex[:8]}"
     arenas = [StateArena(layout, [r], dev) for r in (0, 1)]
-    store = MemoryStore()
-    cks = [PecCheckpointer(layout, arenas[r], store, PecConfig(k_pec=2), "equal_pec", i_ckpt=1,
+    cks = [PecCheckpointer(layout, arenas[r], MemoryStore(), PecConfig(k_pec=2), "equal_pec",
+                           i_ckpt=1,
                            ranks=[r], shared_host_prefix=prefix, async_persist=False)
            for r in (0, 1)]
     try:
