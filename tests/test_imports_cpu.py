@@ -1,0 +1,39 @@
+"""Every `from <package module> import name` in the package, tools and
+bench -- including the lazy ones inside functions, which only run on a GPU
+box or in multi-process mode -- names something that exists (a removed
+helper must fail here, on CPU, not on the GPU box)."""
+
+import ast
+import importlib
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+PKG = "paper_2408_04307_b200"
+FILES = sorted(list((ROOT / PKG).glob("*.py")) + list((ROOT / "tools").glob("*.py")) +
+               [ROOT / "bench.py", ROOT / "__graft_entry__.py",
+                ROOT / "examples" / "moe_training.py"])
+
+
+def _imports(path: Path):
+    tree = ast.parse(path.read_text())
+    for node in ast.walk(tree):
+        if isinstance(node, ast.ImportFrom) and node.module is not None:
+            mod = node.module
+            if node.level:  # relative import inside the package
+                mod = f"{PKG}.{mod}" if mod else PKG
+            if mod == PKG or mod.startswith(PKG + ".") or mod == "oracle" or \
+                    mod.startswith("oracle."):
+                yield mod, [a.name for a in node.names]
+
+
+@pytest.mark.parametrize("path", FILES, ids=lambda p: str(p.relative_to(ROOT)))
+def test_package_imports_resolve(path):
+    for mod, names in _imports(path):
+        m = importlib.import_module(mod)
+        for n in names:
+            if n == "*":
+                continue
+            if not hasattr(m, n):
+                importlib.import_module(f"{mod}.{n}")  # a submodule
