@@ -1,6 +1,6 @@
-"""Every `from <package module> import name` in the package, tools and
-bench -- including the lazy ones inside functions, which only run on a GPU
-box or in multi-process mode -- names something that exists (a removed
+"""Every `from <package module> import name` in the package, tools, tests
+and bench -- including the lazy ones inside functions, which only run on a
+GPU box or in multi-process mode -- names something that exists (a removed
 helper must fail here, on CPU, not on the GPU box)."""
 
 import ast
@@ -12,6 +12,7 @@ import pytest
 ROOT = Path(__file__).resolve().parent.parent
 PKG = "paper_2408_04307_b200"
 FILES = sorted(list((ROOT / PKG).glob("*.py")) + list((ROOT / "tools").glob("*.py")) +
+               list((ROOT / "tests").glob("test_*.py")) +
                [ROOT / "bench.py", ROOT / "__graft_entry__.py",
                 ROOT / "examples" / "moe_training.py"])
 
