@@ -180,6 +180,14 @@ def _crcs(payloads: List, threads: int) -> List[int]:
 PayloadSource = Optional[Mapping[str, object]]
 
 
+def _fsync_path(path) -> None:
+    fd = os.open(str(path), os.O_RDONLY)
+    try:
+        os.fsync(fd)
+    finally:
+        os.close(fd)
+
+
 class DiskStore:
     """One directory per version under ``root`` (store.py:171-282)."""
 
@@ -273,7 +281,17 @@ class DiskStore:
         self._put(tmp, b"", injector)
         if injector is not None:
             injector.charge_op()
+        if self.fsync:
+            # durable before visible: metadata files and every directory
+            # entry reach storage before the COMPLETE rename, the rename after
+            for f in (vdir / "meta.json", vdir / "manifest.tsv", tmp):
+                _fsync_path(f)
+            for d in sorted({(vdir / r).parent for _, r, _, _ in rows} | {vdir}):
+                _fsync_path(d)
         os.replace(tmp, vdir / "COMPLETE")
+        if self.fsync:
+            _fsync_path(vdir)
+            _fsync_path(self.root)
         return StoreManifest(version, iteration, {k: (p, s, c) for k, p, s, c in rows}, True)
 
     def check_version(self, version: int) -> None:
