@@ -13,11 +13,17 @@ from __future__ import annotations
 
 import mmap
 import os
+import weakref
 from typing import Optional
 
 import numpy as np
 
 SHM_DIR = "/dev/shm"
+
+
+def _unregister(addr: int) -> None:
+    import torch
+    torch.cuda.cudart().cudaHostUnregister(addr)
 
 
 def buffer_name(prefix: str, rank: int, buffer_id: int) -> str:
@@ -52,18 +58,23 @@ class SharedHostBuffer:
                 os.close(fd)
         self.array = np.frombuffer(self.mm, dtype=np.uint8)
         self.tensor = torch.from_numpy(self.array) if create else None
-        self.registered = False
+        self._unregister = None
         if create and register:
             rc = torch.cuda.cudart().cudaHostRegister(self.array.ctypes.data, self.nbytes, 0)
             if int(rc) != 0:
                 raise RuntimeError(f"cudaHostRegister({self.path}) failed: {rc}")
-            self.registered = True
+            # unregister even if the owner is dropped without close(): a
+            # mapping freed while registered leaves a stale registration and
+            # the next registration at that address fails (tools/thp_soak.py)
+            self._unregister = weakref.finalize(self, _unregister, self.array.ctypes.data)
+
+    @property
+    def registered(self) -> bool:
+        return self._unregister is not None and self._unregister.alive
 
     def close(self) -> None:
-        import torch
-        if self.registered:
-            torch.cuda.cudart().cudaHostUnregister(self.array.ctypes.data)
-            self.registered = False
+        if self._unregister is not None:
+            self._unregister()
         self.tensor = None
         self.array = None
         try:
