@@ -258,7 +258,7 @@ def prune_store(store, keep: int = 1) -> None:
         shutil.rmtree(store.version_dir(v), ignore_errors=True)
 
 
-def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float, rounds: int = 2):
+def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float, rounds: int = 3):
     """Synthetic per-rank training loop on the compute stream: an F&B proxy
     (bf16 8192^3 GEMMs, calibrated to ~fb_ms) then an update proxy (one
     in-place pass over the whole state arena: HBM-bound like a fused Adam
@@ -327,6 +327,8 @@ def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float, rounds:
             "runs_ms_without": [round(x, 3) for x in runs_without],
             "runs_ms_with": [round(x, 3) for x in runs_with],
             "exposed_ms_per_iter": round(with_ - without, 3),
+            # spread of the baseline runs: differences below it are noise
+            "noise_ms_per_iter": round((max(runs_without) - min(runs_without)) / 2, 3),
             "pack_ms_in_loop": round(statistics.mean(packs), 3) if packs else None,
             "overhead_frac": round((with_ - without) / without, 5)}
 
@@ -773,7 +775,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stall", action="store_true")
-    ap.add_argument("--stall-iters", type=int, default=30)
+    ap.add_argument("--stall-iters", type=int, default=40)
     ap.add_argument("--i-ckpt", type=int, default=10)
     ap.add_argument("--fb-ms", type=float, default=100.0)
     ap.add_argument("--cpu-sample-gb", type=float, default=2.0)
