@@ -257,10 +257,20 @@ class DeviceCheckpointEngine(CheckpointEngine):
                                          chunk_log2=self.chunk_log2)[0] for r in self.ranks]
         table = np.concatenate(tables) if tables else np.zeros(0, dtype=D.DESC_DTYPE)
         total = D.plan_chunks(table, self.chunk_log2)
-        entry = (DeviceTable(table, total, self.device, self.chunk_log2), layouts, region, pos)
+        dt = DeviceTable(table, total, self.device, self.chunk_log2)
+        if self.pack_mode == D.MODE_CRC:
+            self._crc_scratch(dt)   # with the table: no allocation at pack time
+        entry = (dt, layouts, region, pos)
         if key is not None:
             self._tables[key] = entry
         return entry
+
+    def _crc_scratch(self, table: DeviceTable) -> None:
+        import torch
+        if getattr(table, "entry_crc", None) is None:
+            table.chunk_crc = torch.empty(max(1, D.CRC_UNITS_PER_CHUNK * table.total_chunks),
+                                          dtype=torch.int32, device=self.device)
+            table.entry_crc = torch.empty(max(1, table.n), dtype=torch.int32, device=self.device)
 
     DRAIN_PIECE = 256 << 20
 
@@ -276,15 +286,11 @@ class DeviceCheckpointEngine(CheckpointEngine):
     def _launch_pack(self, table: DeviceTable, stream) -> None:
         """pec_pack, or pec_pack_crc in MODE_CRC (per-entry CRCs land in
         table.entry_crc on device)."""
-        import torch
         if self.pack_mode != D.MODE_CRC:
             D.pack(table.tensor, table.n, table.total_chunks, table.chunk_log2, self.pack_mode,
                    stream=stream)
             return
-        if getattr(table, "entry_crc", None) is None:
-            table.chunk_crc = torch.empty(max(1, D.CRC_UNITS_PER_CHUNK * table.total_chunks),
-                                          dtype=torch.int32, device=self.device)
-            table.entry_crc = torch.empty(max(1, table.n), dtype=torch.int32, device=self.device)
+        self._crc_scratch(table)
         D.pack_crc(table.tensor, table.n, table.total_chunks, table.chunk_crc, table.entry_crc,
                    table.chunk_log2, stream=stream)
 
