@@ -152,7 +152,7 @@ def train(iters: int = 30, i_ckpt: int = 5, store_root=None, seed: int = 0, toke
     store = DiskStore(store_root or tempfile.mkdtemp(prefix="pec_example_"))
     pec = PecConfig(k_pec=2, selection="load_aware", k_snapshot=2, k_persist=1)
     ck = PecCheckpointer(layout, arena, store, pec, "equal_pec", i_ckpt=i_ckpt, counters=counters)
-    ck.engine.reserve(ck.max_snapshot_bytes())
+    ck.prepare()                       # staging + pinned host buffers + phase tables
     g = torch.Generator(device=dev)
     losses = []
     it = 1

@@ -700,6 +700,17 @@ class PecCheckpointer:
                     else plan_equal(self.layout, seq)
         return self._plan
 
+    def prepare(self, host_buffers: Optional[int] = None) -> None:
+        """Do the start-up work once, before training: allocate the HBM
+        staging buffer and pin the host snapshot buffers (pinning runs at a
+        few GB/s), and build every phase's device descriptor table of a
+        periodic (sequential) plan, so no checkpoint plans or allocates."""
+        self.engine.reserve(self.max_snapshot_bytes(), host_buffers=host_buffers)
+        plan = self.plan()
+        if plan is not None:
+            for p in range(plan.period):
+                self.engine.layouts_for(plan.assignments[p], ("phase", p))
+
     def max_snapshot_bytes(self) -> int:
         """Upper bound of this process's staging bytes over all phases."""
         plan = self.plan()

@@ -41,7 +41,8 @@ def test_toy_sequential_chain_persists_exact_bytes(dev, tmp_path):
     arena = StateArena(layout, [0], dev, w.expert_tensors)
     store = DiskStore(tmp_path)
     ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=5)
-    ck.engine.reserve(ck.max_snapshot_bytes())
+    ck.prepare()        # staging, pinned buffers and every phase's table up front
+    assert len(ck.engine._tables) == ck.plan().period
     expected = {}
     for it in range(1, 31):
         _mutate(arena, it)  # "optimizer step" of iteration it
