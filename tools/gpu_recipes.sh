@@ -70,6 +70,12 @@ case "$recipe" in
       --master-addr 127.0.0.1 --master-port 29553 bench.py --impl reference --gpus $N \
       --steps 2 --warmup 1 2>/dev/null | tail -1 > $O/bench_n${N}_ref.json
     ;;
+  soak)   # the GPU suite N times (flake hunting); prints one summary line per run
+    N=${2:-10}
+    for i in $(seq 1 $N); do
+      timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -E "passed|failed|^E " | head -6
+    done
+    ;;
   *)
     echo "unknown recipe: $recipe" >&2; exit 2 ;;
 esac
