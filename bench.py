@@ -162,22 +162,24 @@ def host_buffers_that_fit(nbytes: int, want: int, frac: float = 0.7) -> int:
 # ---------------------------------------------------------------------------
 
 def cpu_pack_sample(entries, sample_bytes: int, threads: int, min_seconds: float):
-    """Pack a bounded sample of this rank's planned ranges (first entries in
-    plan order, truncated to `sample_bytes`) from a host-resident state image
-    with the oracle's threaded numpy restatement; repeat until
+    """Pack a bounded sample of this rank's planned ranges from a
+    host-resident state image with the oracle's threaded numpy restatement:
+    every entry of the plan, each cut to the same fraction of its length
+    (sample_bytes / total; at least 256 B), so the sample keeps the
+    workload's mix of entry sizes and alignments.  Repeat until
     `min_seconds` of CPU work.  Returns (GB/s of payload, description)."""
     from oracle import pec_oracle as O
-    copies, src_pos, dst_pos, left = [], 0, 0, sample_bytes
+    entries = [e for e in entries if e.nbytes > 0]
+    total = sum(e.nbytes for e in entries)
+    frac = min(1.0, sample_bytes / max(1, total))
+    copies, src_pos, dst_pos = [], 0, 0
     for e in entries:
-        n = min(e.nbytes, left)
-        if n <= 0:
-            break
+        n = min(e.nbytes, max(256, int(e.nbytes * frac)))
         src = src_pos + (e.src_offset % 256)
         dst = dst_pos + ((src - dst_pos) % 256)
         copies.append((src, dst, n))
         src_pos = src + n + 256
         dst_pos = dst + n
-        left -= n
     state = np.random.default_rng(0).integers(0, 256, size=src_pos + 256, dtype=np.uint8)
     out = np.empty(dst_pos + 256, dtype=np.uint8)
     payload = sum(c[2] for c in copies)
@@ -190,8 +192,9 @@ def cpu_pack_sample(entries, sample_bytes: int, threads: int, min_seconds: float
         if time.perf_counter() - t0 >= min_seconds:
             break
     dt = time.perf_counter() - t0
-    desc = (f"oracle numpy pack of the first {payload / 1e9:.2f} GB of rank ranges "
-            f"({len(copies)} entries) x{reps} passes, {threads} threads")
+    desc = (f"oracle numpy pack of {payload / 1e9:.2f} GB: every one of the rank's "
+            f"{len(copies)} planned entries cut to {100 * frac:.1f} % of its length, "
+            f"x{reps} passes, {threads} threads")
     return payload * reps / dt / 1e9, desc
 
 
