@@ -69,6 +69,11 @@ int pec_token_hist(const int32_t* idx, int L, int64_t n_per_layer, int E,
                    const int64_t* cap, int64_t* counters, int tiers,
                    int64_t* delivered, uint32_t* scratch, void* stream);
 
+/* Same with int64 ids (torch.topk's index dtype: no conversion pass). */
+int pec_token_hist_i64(const int64_t* idx, int L, int64_t n_per_layer, int E,
+                       const int64_t* cap, int64_t* counters, int tiers,
+                       int64_t* delivered, uint32_t* scratch, void* stream);
+
 /* ---- (b) K_pec expert selection --------------------------------------- *
  * Replaces: select_window / select_sequential (selector.py:21-32).
  * Writes, for each layer m, the set {(m + c*stride + j) mod E : j < width}

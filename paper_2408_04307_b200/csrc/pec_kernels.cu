@@ -43,8 +43,9 @@ using pecdev::sm_count;
 constexpr int kHistThreads = 256;
 constexpr int kHistUnroll = 8;
 
+template <typename Id>
 __global__ void __launch_bounds__(kHistThreads)
-token_hist_kernel(const int32_t* __restrict__ idx, int L, int64_t n, int E,
+token_hist_kernel(const Id* __restrict__ idx, int L, int64_t n, int E,
                   const int64_t* __restrict__ cap, int64_t* __restrict__ counters,
                   int tiers, int64_t* __restrict__ delivered,
                   uint32_t* __restrict__ scratch) {
@@ -56,21 +57,22 @@ token_hist_kernel(const int32_t* __restrict__ idx, int L, int64_t n, int E,
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = (int64_t)blockIdx.x * per;
   const int64_t hi = lo + per < n ? lo + per : n;
-  const int32_t* row = idx + (int64_t)layer * n;
+  const Id* row = idx + (int64_t)layer * n;
   const unsigned lane = threadIdx.x & 31u;
 
   // The trip count depends only on (lo, hi), uniform across the CTA, so the
   // full-mask __match_any_sync below always sees converged warps.
   for (int64_t base = lo; base < hi; base += (int64_t)kHistThreads * kHistUnroll) {
-    int v[kHistUnroll];
+    Id v[kHistUnroll];
 #pragma unroll
     for (int u = 0; u < kHistUnroll; ++u) {
       const int64_t i = base + (int64_t)u * kHistThreads + threadIdx.x;
-      v[u] = i < hi ? __ldg(row + i) : -1;
+      v[u] = i < hi ? __ldg(row + i) : Id(-1);
     }
 #pragma unroll
     for (int u = 0; u < kHistUnroll; ++u) {
-      const int key = (unsigned)v[u] < (unsigned)E ? v[u] : E;
+      // ids outside [0, E) (dropped tokens, any width) go to the ignore slot
+      const int key = (v[u] >= 0 && v[u] < (Id)E) ? (int)v[u] : E;
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       if (lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[key], (uint32_t)__popc(peers));
     }
@@ -684,6 +686,28 @@ int launch_copy(const pec_copy_desc* descs, int n, uint64_t total, const uint64_
   }
 }
 
+template <typename Id>
+int launch_token_hist(const Id* idx, int L, int64_t n_per_layer, int E, const int64_t* cap,
+                      int64_t* counters, int tiers, int64_t* delivered, uint32_t* scratch,
+                      void* stream) {
+  if (L < 1 || L > 65535 || E < 1 || n_per_layer < 0 || tiers < 0) return PEC_E_INVAL;
+  if (E > kMaxExperts) return PEC_E_RANGE;
+  if (scratch == nullptr || (n_per_layer > 0 && idx == nullptr)) return PEC_E_INVAL;
+  if (tiers > 0 && counters == nullptr) return PEC_E_INVAL;
+  const int sms = sm_count();
+  // enough CTAs to fill the GPU, each with >= one full unrolled sweep of ids
+  int64_t per_layer = (int64_t)sms * 4 / L;
+  const int64_t sweep = (int64_t)kHistThreads * kHistUnroll;
+  const int64_t need = (n_per_layer + sweep - 1) / sweep;
+  if (per_layer > need) per_layer = need;
+  if (per_layer < 1) per_layer = 1;
+  dim3 grid((unsigned)per_layer, (unsigned)L);
+  const size_t smem = (size_t)(E + 1) * sizeof(uint32_t);
+  token_hist_kernel<Id><<<grid, kHistThreads, smem, as_stream(stream)>>>(
+      idx, L, n_per_layer, E, cap, counters, tiers, delivered, scratch);
+  return launch_status();
+}
+
 }  // namespace
 
 // ========================================================================
@@ -707,22 +731,15 @@ const char* pec_strerror(int code) {
 int pec_token_hist(const int32_t* idx, int L, int64_t n_per_layer, int E,
                    const int64_t* cap, int64_t* counters, int tiers,
                    int64_t* delivered, uint32_t* scratch, void* stream) {
-  if (L < 1 || L > 65535 || E < 1 || n_per_layer < 0 || tiers < 0) return PEC_E_INVAL;
-  if (E > kMaxExperts) return PEC_E_RANGE;
-  if (scratch == nullptr || (n_per_layer > 0 && idx == nullptr)) return PEC_E_INVAL;
-  if (tiers > 0 && counters == nullptr) return PEC_E_INVAL;
-  const int sms = sm_count();
-  // enough CTAs to fill the GPU, each with >= one full unrolled sweep of ids
-  int64_t per_layer = (int64_t)sms * 4 / L;
-  const int64_t sweep = (int64_t)kHistThreads * kHistUnroll;
-  const int64_t need = (n_per_layer + sweep - 1) / sweep;
-  if (per_layer > need) per_layer = need;
-  if (per_layer < 1) per_layer = 1;
-  dim3 grid((unsigned)per_layer, (unsigned)L);
-  const size_t smem = (size_t)(E + 1) * sizeof(uint32_t);
-  token_hist_kernel<<<grid, kHistThreads, smem, as_stream(stream)>>>(
-      idx, L, n_per_layer, E, cap, counters, tiers, delivered, scratch);
-  return launch_status();
+  return launch_token_hist(idx, L, n_per_layer, E, cap, counters, tiers, delivered, scratch,
+                           stream);
+}
+
+int pec_token_hist_i64(const int64_t* idx, int L, int64_t n_per_layer, int E,
+                       const int64_t* cap, int64_t* counters, int tiers,
+                       int64_t* delivered, uint32_t* scratch, void* stream) {
+  return launch_token_hist(idx, L, n_per_layer, E, cap, counters, tiers, delivered, scratch,
+                           stream);
 }
 
 int pec_select_sequential(int64_t c, int L, int E, int width, int stride,

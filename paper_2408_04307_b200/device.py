@@ -59,6 +59,7 @@ def _load():
         "pec_abi_version": (c_int, []),
         "pec_strerror": (ctypes.c_char_p, [c_int]),
         "pec_token_hist": (c_int, [vp, c_int, c_i64, c_int, vp, vp, c_int, vp, vp, vp]),
+        "pec_token_hist_i64": (c_int, [vp, c_int, c_i64, c_int, vp, vp, c_int, vp, vp, vp]),
         "pec_select_sequential": (c_int, [c_i64, c_int, c_int, c_int, c_int, vp, vp]),
         "pec_select_load_aware": (c_int, [vp, c_int, c_int, c_int, vp, c_int, vp, c_int, vp]),
         "pec_pack": (c_int, [vp, c_int, c_u64, c_int, c_int, vp]),
@@ -90,7 +91,8 @@ def lib():
 
 def exported_symbols():
     """Names declared in include/pec.h (for the ABI tests)."""
-    return ["pec_abi_version", "pec_strerror", "pec_token_hist", "pec_select_sequential",
+    return ["pec_abi_version", "pec_strerror", "pec_token_hist", "pec_token_hist_i64",
+            "pec_select_sequential",
             "pec_select_load_aware", "pec_pack", "pec_unpack", "pec_plan_chunks",
             "pec_expand_plan", "pec_pack_indirect", "pec_pack_crc",
             "pec_crc32c", "pec_crc32c_combine", "pec_crc32c_many", "pec_write_files"]
@@ -137,8 +139,9 @@ def _dev_ptr(t, dtype, what: str, ndim: Optional[int] = None) -> int:
 
 def token_hist(idx, counters, scratch, cap=None, delivered=None, stream=None) -> None:
     """counters[t] += min(bincount(idx[l]), cap[l]) for every tier t
-    (pec_token_hist).  idx [L, n] int32, counters [tiers, L, E] int64,
-    scratch [L*E+1] int32 zeros (reused), cap [L] int64, delivered [L, E]."""
+    (pec_token_hist / pec_token_hist_i64).  idx [L, n] int32 or int64 (as
+    torch.topk returns it), counters [tiers, L, E] int64, scratch [L*E+1]
+    int32 zeros (reused), cap [L] int64, delivered [L, E]."""
     import torch
     L, n = idx.shape
     tiers, L2, E = counters.shape
@@ -148,10 +151,11 @@ def token_hist(idx, counters, scratch, cap=None, delivered=None, stream=None) ->
         raise SpecValidationError("scratch.numel() >= L*E+1", f"got {scratch.numel()}")
     cap_p = _dev_ptr(cap, torch.int64, "cap", 1) if cap is not None else None
     del_p = _dev_ptr(delivered, torch.int64, "delivered", 2) if delivered is not None else None
-    rc = lib().pec_token_hist(_dev_ptr(idx, torch.int32, "idx", 2), L, n, E, cap_p,
-                              _dev_ptr(counters, torch.int64, "counters", 3), tiers, del_p,
-                              _dev_ptr(scratch, torch.int32, "scratch"),
-                              _stream_handle(stream, idx.device))
+    wide = idx.dtype == torch.int64
+    fn = lib().pec_token_hist_i64 if wide else lib().pec_token_hist
+    rc = fn(_dev_ptr(idx, torch.int64 if wide else torch.int32, "idx", 2), L, n, E, cap_p,
+            _dev_ptr(counters, torch.int64, "counters", 3), tiers, del_p,
+            _dev_ptr(scratch, torch.int32, "scratch"), _stream_handle(stream, idx.device))
     _check(rc, "pec_token_hist")
 
 

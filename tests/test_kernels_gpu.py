@@ -40,6 +40,31 @@ def test_token_hist_matches_bincount_with_cap(dev, L, n, E):
     assert int(scratch.abs().sum()) == 0  # left zeroed for the next call
 
 
+def test_token_hist_accepts_int64_ids(dev):
+    """torch.topk returns int64 indices: pec_token_hist_i64 counts them
+    directly -- equal to the int32 path, and ids outside [0, E) in any width
+    (negative, >= E, >= 2^31) are dropped, never aliased into range."""
+    import torch
+    from paper_2408_04307_b200 import device as D
+    rng = np.random.default_rng(64)
+    L, n, E = 3, 50_000, 16
+    ids = rng.integers(0, E, size=(L, n)).astype(np.int64)
+    ids[0, :7] = [-1, E, 2 ** 31 + 3, 2 ** 32 + 5, -(2 ** 40), 2 ** 33, E - 1]
+    cap = np.array([O.capacity(1.25, n, E)] * L, dtype=np.int64)
+    out = []
+    for dt in (torch.int64, torch.int32):
+        t = torch.from_numpy(ids).to(dev)
+        if dt == torch.int32:
+            t = torch.where((t >= 0) & (t < E), t, torch.full_like(t, -1)).to(torch.int32)
+        counters = torch.zeros((1, L, E), dtype=torch.int64, device=dev)
+        scratch = torch.zeros(L * E + 1, dtype=torch.int32, device=dev)
+        D.token_hist(t, counters, scratch, cap=torch.from_numpy(cap).to(dev))
+        out.append(counters[0].cpu().numpy())
+    assert np.array_equal(out[0], out[1])
+    clean = np.where((ids >= 0) & (ids < E), ids, -1)
+    assert np.array_equal(out[0], O.route_counts(clean, E, cap))
+
+
 def test_token_hist_reproduces_reference_zipf_routing(dev):
     """Explicit ids drawn from the reference's PCG64 Zipf stream, counted on
     device, equal the reference route_tokens counts (golden)."""
