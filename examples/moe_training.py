@@ -87,7 +87,7 @@ def forward(params, shp, tokens, targets):
         h = F.layer_norm(x, (d,), ln2[:d], ln2[d:])
         logits = h @ P(f"l{layer}_gate").view(d, E)
         weights, ids = torch.topk(torch.softmax(logits, -1), k, dim=-1)   # [T, k]
-        router_ids.append(ids.reshape(-1).to(torch.int32))
+        router_ids.append(ids.reshape(-1))               # int64, counted as is
         out = torch.zeros_like(h)
         for e in range(E):
             sel = (ids == e)
@@ -102,7 +102,7 @@ def forward(params, shp, tokens, targets):
     lnf = P("lnf")
     x = F.layer_norm(x, (d,), lnf[:d], lnf[d:])
     loss = F.cross_entropy(x @ emb.t(), targets)
-    return loss, torch.stack(router_ids)                 # ids [L, T*k]
+    return loss, torch.stack(router_ids)                 # ids [L, T*k] int64
 
 
 def adam_step(params, step: int, lr=3e-3, b1=0.9, b2=0.999, eps=1e-8):
