@@ -143,6 +143,8 @@ def token_hist(idx, counters, scratch, cap=None, delivered=None, stream=None) ->
     torch.topk returns it), counters [tiers, L, E] int64, scratch [L*E+1]
     int32 zeros (reused), cap [L] int64, delivered [L, E]."""
     import torch
+    if idx.dim() == 3 and idx.is_contiguous():   # [L, tokens, top_k] as stacked topk output
+        idx = idx.view(idx.shape[0], -1)
     L, n = idx.shape
     tiers, L2, E = counters.shape
     if L2 != L:

@@ -63,6 +63,12 @@ def test_token_hist_accepts_int64_ids(dev):
     assert np.array_equal(out[0], out[1])
     clean = np.where((ids >= 0) & (ids < E), ids, -1)
     assert np.array_equal(out[0], O.route_counts(clean, E, cap))
+    # [L, tokens, top_k] (stacked topk indices) is accepted as is
+    counters = torch.zeros((1, L, E), dtype=torch.int64, device=dev)
+    scratch = torch.zeros(L * E + 1, dtype=torch.int32, device=dev)
+    D.token_hist(torch.from_numpy(ids).to(dev).view(L, n // 2, 2), counters, scratch,
+                 cap=torch.from_numpy(cap).to(dev))
+    assert np.array_equal(counters[0].cpu().numpy(), out[0])
 
 
 def test_token_hist_reproduces_reference_zipf_routing(dev):
