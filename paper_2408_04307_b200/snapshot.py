@@ -210,8 +210,8 @@ class DeviceCheckpointEngine(CheckpointEngine):
             shb = SharedHostBuffer(buffer_name(self.shared_prefix, rank, bid), create=False,
                                    register=False)
             st = StagingLayout.build(buf.content.get(rank, ()), PeerSlots(self.layout, rank), rank)
-            # the owner publishes its region size, rounded up to 256 B
-            if (st.nbytes + 255) // 256 * 256 != meta["nbytes"]:
+            # the owner publishes its region size (host plans round it up to 256 B)
+            if meta["nbytes"] not in (st.nbytes, (st.nbytes + 255) // 256 * 256):
                 raise RuntimeError(f"peer rank {rank} v{version}: layout size mismatch "
                                    f"({st.nbytes} B vs {meta['nbytes']} B published)")
             return shb, st
@@ -273,6 +273,11 @@ class DeviceCheckpointEngine(CheckpointEngine):
             table.entry_crc = torch.empty(max(1, table.n), dtype=torch.int32, device=self.device)
 
     DRAIN_PIECE = 256 << 20
+
+    def _drain_range(self, host, start: int, stop: int) -> None:
+        for o in range(start, stop, self.DRAIN_PIECE):
+            e = min(stop, o + self.DRAIN_PIECE)
+            host[o:e].copy_(self.staging[o:e], non_blocking=True)
 
     def _drain(self, host, nbytes: int) -> None:
         """Staging -> pinned host copy of the snapshot, enqueued on the current
@@ -352,43 +357,60 @@ class DeviceCheckpointEngine(CheckpointEngine):
 
     # -- device-planned snapshots (load-aware: no host round trip before the pack)
     def enable_device_plans(self, strategy: str) -> None:
-        """Build this rank's all-experts template once; afterwards
-        `begin_snapshot_device` expands the plan on the GPU from a device
-        selection (equal_pec / baseline; one local rank)."""
+        """Build each local rank's all-experts template once; afterwards
+        `begin_snapshot_device` expands the plans on the GPU from a device
+        selection (equal_pec / baseline).  Each local rank owns a fixed
+        staging region sized for its largest possible plan, so the regions
+        never move whatever the selection."""
         import torch
-        if len(self.ranks) != 1:
-            raise ValueError("device plans need exactly one local rank per engine")
         self.strategy = strategy
-        self.template = PlanTemplate(self.layout, self.arena, self.ranks[0], strategy, self.device)
-        self._ensure_staging(self.template.max_bytes)
-        self._dev_table = torch.empty(max(1, self.template.n) * 4, dtype=torch.int64,
-                                      device=self.device)
-        self._dev_totals = torch.zeros(2, dtype=torch.int64, device=self.device)
+        self.templates = {r: PlanTemplate(self.layout, self.arena, r, strategy, self.device)
+                          for r in self.ranks}
+        self.template = self.templates[self.ranks[0]]       # the single-rank case
+        self._dev_region, pos = {}, 0
+        for r in self.ranks:
+            self._dev_region[r] = pos
+            pos += (self.templates[r].max_bytes + 255) // 256 * 256
+        self._dev_region_bytes = pos
+        self._ensure_staging(pos)
+        self._dev_tables = {r: torch.empty(max(1, t.n) * 4, dtype=torch.int64, device=self.device)
+                            for r, t in self.templates.items()}
+        self._dev_totals_r = {r: torch.zeros(2, dtype=torch.int64, device=self.device)
+                              for r in self.ranks}
+        self._dev_table = self._dev_tables[self.ranks[0]]   # single-rank names (bench, tools)
+        self._dev_totals = self._dev_totals_r[self.ranks[0]]
         self._meta_stream = torch.cuda.Stream(device=self.device)
 
     def _expand_and_pack(self, snap_sel_dev, stream):
         import torch
-        t = self.template
-        D.expand_plan(t.tensor, t.n, snap_sel_dev, self.arena.base_address,
-                      self.staging.data_ptr(), self._dev_table, self._dev_totals,
-                      self.chunk_log2, stream=stream)
+        lg = self.chunk_log2
+        for r in self.ranks:
+            t = self.templates[r]
+            D.expand_plan(t.tensor, t.n, snap_sel_dev, self.arena.base_address,
+                          self.staging.data_ptr() + self._dev_region[r], self._dev_tables[r],
+                          self._dev_totals_r[r], lg, stream=stream)
         expanded = torch.cuda.Event()
         expanded.record(stream)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        if self.pack_mode == D.MODE_CRC:
-            if getattr(self, "_dev_entry_crc", None) is None:
-                self._dev_chunk_crc = torch.empty(
-                    max(1, D.CRC_UNITS_PER_CHUNK * t.max_chunks(self.chunk_log2)),
-                    dtype=torch.int32, device=self.device)
-                self._dev_entry_crc = torch.empty(max(1, t.n), dtype=torch.int32,
-                                                  device=self.device)
-            D.pack_crc(self._dev_table, t.n, t.max_chunks(self.chunk_log2), self._dev_chunk_crc,
-                       self._dev_entry_crc, self.chunk_log2, stream=stream,
-                       totals_dev=self._dev_totals)
-        else:
-            D.pack_indirect(self._dev_table, t.n, t.max_chunks(self.chunk_log2),
-                            self._dev_totals, self.chunk_log2, self.pack_mode, stream=stream)
+        if self.pack_mode == D.MODE_CRC and getattr(self, "_dev_entry_crc_r", None) is None:
+            self._dev_chunk_crc_r = {
+                r: torch.empty(max(1, D.CRC_UNITS_PER_CHUNK * t.max_chunks(lg)),
+                               dtype=torch.int32, device=self.device)
+                for r, t in self.templates.items()}
+            self._dev_entry_crc_r = {r: torch.empty(max(1, t.n), dtype=torch.int32,
+                                                    device=self.device)
+                                     for r, t in self.templates.items()}
+            self._dev_entry_crc = self._dev_entry_crc_r[self.ranks[0]]
+        for r in self.ranks:
+            t = self.templates[r]
+            if self.pack_mode == D.MODE_CRC:
+                D.pack_crc(self._dev_tables[r], t.n, t.max_chunks(lg), self._dev_chunk_crc_r[r],
+                           self._dev_entry_crc_r[r], lg, stream=stream,
+                           totals_dev=self._dev_totals_r[r])
+            else:
+                D.pack_indirect(self._dev_tables[r], t.n, t.max_chunks(lg), self._dev_totals_r[r],
+                                lg, self.pack_mode, stream=stream)
         t1.record(stream)
         return expanded, t0, t1
 
@@ -424,15 +446,20 @@ class DeviceCheckpointEngine(CheckpointEngine):
         expanded, t0, t1 = self._expand_and_pack(snap_sel_dev, ps)
         # small D2H of {chunks, bytes} and both selections on a side stream
         ms.wait_event(expanded)
-        meta = torch.empty(2 + snap_sel_dev.numel() + persist_sel_dev.numel(), dtype=torch.int64,
-                           pin_memory=True)
+        R = len(self.ranks)
+        head = 2 * R
+        meta = torch.empty(head + snap_sel_dev.numel() + persist_sel_dev.numel(),
+                           dtype=torch.int64, pin_memory=True)
         with torch.cuda.stream(ms):
-            meta[:2].copy_(self._dev_totals, non_blocking=True)
-            meta[2:2 + snap_sel_dev.numel()].copy_(snap_sel_dev.reshape(-1), non_blocking=True)
-            meta[2 + snap_sel_dev.numel():].copy_(persist_sel_dev.reshape(-1), non_blocking=True)
+            for i, r in enumerate(self.ranks):
+                meta[2 * i:2 * i + 2].copy_(self._dev_totals_r[r], non_blocking=True)
+            meta[head:head + snap_sel_dev.numel()].copy_(snap_sel_dev.reshape(-1),
+                                                         non_blocking=True)
+            meta[head + snap_sel_dev.numel():].copy_(persist_sel_dev.reshape(-1),
+                                                     non_blocking=True)
         ready = torch.cuda.Event()
         ready.record(ms)
-        rec = _Inflight({}, {self.ranks[0]: 0}, 0, t_begin=time.perf_counter())
+        rec = _Inflight({}, dict(self._dev_region), 0, t_begin=time.perf_counter())
         rec.pack_start, rec.pack_done = t0, t1
         rec.pending = (meta, ready, snap_sel_dev.shape[0], snap_sel_dev.numel())
         self._inflight[buf.buffer_id] = rec
@@ -453,34 +480,49 @@ class DeviceCheckpointEngine(CheckpointEngine):
         if not block and not ready.query():
             return False
         ready.synchronize()
-        rank = self.ranks[0]
         buf = self.buffers.buffers[bid]
-        nbytes = int(meta[1])
-        snap_h = meta[2:2 + n_snap].view(L, -1).tolist()
-        pers_h = meta[2 + n_snap:].view(L, -1).tolist()
+        head = 2 * len(self.ranks)
+        snap_h = meta[head:head + n_snap].view(L, -1).tolist()
+        pers_h = meta[head + n_snap:].view(L, -1).tolist()
         due = {m: frozenset(e for e in snap_h[m] if e >= 0) for m in range(L)}
         rec.persist_due = {m: frozenset(e for e in pers_h[m] if e >= 0) for m in range(L)}
         assignment = build_phase_assignment(self.layout, due, self.strategy)
         buf.content = assignment
-        layout = StagingLayout.build(assignment.get(rank, ()), self.arena, rank)
-        if layout.nbytes != nbytes:
-            raise RuntimeError(f"device plan ({nbytes} B) disagrees with host plan "
-                               f"({layout.nbytes} B)")
-        host = self._ensure_host(bid, nbytes)
-        rec.layouts, rec.nbytes = {rank: layout}, nbytes
+        layouts, used = {}, {}
+        for i, r in enumerate(self.ranks):
+            st = StagingLayout.build(assignment.get(r, ()), self.arena, r)
+            used[r] = int(meta[2 * i + 1])
+            if st.nbytes != used[r]:
+                raise RuntimeError(f"device plan of rank {r} ({used[r]} B) disagrees with the "
+                                   f"host plan ({st.nbytes} B)")
+            layouts[r] = st
+        last = self.ranks[-1]
+        nbytes = self._dev_region[last] + used[last]
+        host = self._ensure_host(bid, self._dev_region_bytes)
+        rec.layouts, rec.nbytes = layouts, nbytes
         cs = self.copy_stream
         cs.wait_event(rec.pack_done)
         rec.drain_done = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(cs):
-            self._drain(host, nbytes)
-            if self.pack_mode == D.MODE_CRC and self.template.n:
-                # template order; dropped entries carry nbytes 0 (crc 0)
-                rec.entry_crc = torch.empty(self.template.n, dtype=torch.int32, pin_memory=True)
-                rec.entry_crc.copy_(self._dev_entry_crc[:self.template.n], non_blocking=True)
-                rec.crc_keys = [a.store_key for a in self.template.ranges]
+            for r in self.ranks:        # each region's used bytes only
+                o = self._dev_region[r]
+                self._drain_range(host, o, o + used[r])
+            if self.pack_mode == D.MODE_CRC:
+                # template order per rank; dropped entries carry nbytes 0 (crc 0)
+                total_n = sum(t.n for t in self.templates.values())
+                if total_n:
+                    rec.entry_crc = torch.empty(total_n, dtype=torch.int32, pin_memory=True)
+                    o, keys = 0, []
+                    for r in self.ranks:
+                        t = self.templates[r]
+                        rec.entry_crc[o:o + t.n].copy_(self._dev_entry_crc_r[r][:t.n],
+                                                       non_blocking=True)
+                        keys += [a.store_key for a in t.ranges]
+                        o += t.n
+                    rec.crc_keys = keys
         rec.drain_done.record(cs)
         self._staging_free = rec.drain_done
-        self.stats["snap_bytes"].append(layout.payload_bytes)
+        self.stats["snap_bytes"].append(sum(st.payload_bytes for st in layouts.values()))
         rec.pending = None
         self._pending_bid = None
         return True
@@ -683,9 +725,8 @@ class PecCheckpointer:
                                           "load-aware selection is not periodic")
             if counters is None:
                 raise ValueError("load-aware selection needs DeviceTokenCounters")
-            if len(self.engine.ranks) == 1:
-                self.engine.enable_device_plans(strategy)
-                self.device_plans = True
+            self.engine.enable_device_plans(strategy)
+            self.device_plans = True
 
     # -- plans --------------------------------------------------------------------
     def plan(self) -> Optional[ShardPlan]:

@@ -417,6 +417,52 @@ def test_memory_restore_from_a_peer_engines_node_shared_buffer(dev, tmp_path):
     assert not [f for f in os.listdir("/dev/shm") if f.startswith(prefix)]
 
 
+@pytest.mark.parametrize("pack_mode", [0, 3])
+def test_device_plans_for_several_local_ranks(dev, tmp_path, pack_mode):
+    """Load-aware device plans with four ranks in one engine (fixed per-rank
+    staging regions, one expand + pack per rank, per-region drains), in the
+    plain and the CRC-computing engine: persisted versions read back
+    CRC-verified and equal to the state at snapshot time."""
+    import torch
+    from paper_2408_04307_b200 import PecConfig
+    from paper_2408_04307_b200.arena import StateArena
+    from paper_2408_04307_b200.counting import DeviceTokenCounters
+    from paper_2408_04307_b200.snapshot import PecCheckpointer
+    from paper_2408_04307_b200.store import DiskStore
+    layout = make_layout(n_experts=8, n_layers=2, dp=4, ep=2, gpus_per_node=2, epp=30_001,
+                         other=77)
+    ranks = list(range(4))
+    arena = StateArena(layout, ranks, dev)
+    L, E = 2, 8
+    counters = DeviceTokenCounters(L, E, dev)
+    pec = PecConfig(k_pec=3, selection="load_aware", k_snapshot=3, k_persist=2)
+    ck = PecCheckpointer(layout, arena, DiskStore(tmp_path), pec, "equal_pec", i_ckpt=1,
+                         ranks=ranks, counters=counters, pack_mode=pack_mode)
+    assert ck.device_plans and len(ck.engine.templates) == 4
+    ck.prepare()
+    shadow = {}
+    gen = torch.Generator(device=dev).manual_seed(11)
+    for it in range(1, 6):
+        _mutate(arena, it)
+        ids = torch.randint(0, E, (L, 300), dtype=torch.int64, device=dev, generator=gen)
+        buf = ck.step(it, ids)
+        torch.cuda.synchronize()
+        shadow[buf.version] = arena.buffer.cpu().numpy().copy()
+        ck.wait_pack()
+    ck.finish()
+    vs = ck.engine.store.complete_versions()
+    assert vs == sorted(shadow)
+    for v in vs:
+        data = ck.engine.store.load_checkpoint(v)      # CRC-verified read
+        meta = ck.engine.store.meta(v)
+        assert {e.rank for e in meta.entries.values()} == set(ranks)
+        for sk, b in data.items():
+            e = meta.entries[sk]
+            off = arena.slot(e.unit_key).offset + e.start
+            assert b == shadow[v][off:off + e.stop - e.start].tobytes(), (v, sk)
+    ck.close()
+
+
 @pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
 def test_gpt350m_k_sweep_pack_bit_exact_on_device(dev, k):
     """K_pec sweep on GPT-MoE 350M-16E (dp=8 x ep=8, ranks 0..7 emulated):
