@@ -55,6 +55,9 @@ case "$recipe" in
     timeout 300 python tools/d2h_probe.py > $O/d2h_probe.json 2>&1; cat $O/d2h_probe.json
     timeout 300 python tools/d2h_push_probe.py > $O/d2h_push_probe.json 2>&1
     ;;
+  stall_law)   # the reference's stall law vs measured stalls over an F&B sweep (Mixtral rank)
+    timeout 900 python tools/stall_law_probe.py > $O/stall_law.json 2> $O/stall_law.err; cat $O/stall_law.json
+    ;;
   chain)   # config 5: PEC chain + node fault + restore + K sweep
     timeout 1200 python tools/restore_chain.py --k 1 > $O/restore_chain_k1.json 2> $O/restore_chain.err
     echo chain=$?
