@@ -80,10 +80,23 @@ __device__ __forceinline__ uint32_t shift_bytes(const uint32_t* x2k, uint32_t r,
   return n ? gf2_mul(xpow_bytes(x2k, n), r) : r;
 }
 
-__device__ __forceinline__ uint32_t fold_word(const uint32_t* tab, uint32_t c, uint32_t w) {
+// Byte-table lookup at the lane-replicated slot: entry e of lane l is word
+// 32e + l, i.e. byte offset (e << 7) | (l << 2) from the table base, formed by
+// one shift and one LOP3 ((c << 7) & 0x7F80 | lane4).  The table is a static
+// shared array, so its base is an immediate of the LDS (no per-lookup add),
+// and the LOP3 is opaque so the compiler cannot re-associate lane4 into a
+// base register.
+__device__ __forceinline__ uint32_t lut(const uint32_t* table, uint32_t c, uint32_t lane4) {
+  uint32_t off;
+  asm("lop3.b32 %0, %1, 0x7F80, %2, 0xEA;" : "=r"(off) : "r"(c << 7), "r"(lane4));
+  return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(table) + off);
+}
+
+__device__ __forceinline__ uint32_t fold_word(const uint32_t* table, uint32_t lane4, uint32_t c,
+                                              uint32_t w) {
   c ^= w;
 #pragma unroll
-  for (int b = 0; b < 4; ++b) c = tab[(c & 0xFFu) << 5] ^ (c >> 8);
+  for (int b = 0; b < 4; ++b) c = lut(table, c, lane4) ^ (c >> 8);
   return c;
 }
 
@@ -111,7 +124,7 @@ constexpr int kLaneTabWords = 8 * 16 * 32;  // per-lane x^(8*P*(31-l)) windows
 
 template <int kThreads, int kSub, bool kLaneMul>
 constexpr int pack_crc_smem() {
-  return (kTableWords + (kLaneMul ? 2 * 128 : kPackMulWords) + (kLaneMul ? kLaneTabWords : 0)) * 4 +
+  return ((kLaneMul ? 2 * 128 : kPackMulWords) + (kLaneMul ? kLaneTabWords : 0)) * 4 +
          (kThreads / 32) * (4096 / kSub);
 }
 
@@ -128,10 +141,11 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
   constexpr int kVecSub = kVecPerThread / kSub;   // 16-byte vectors per lane per round
   constexpr int kChains = 4 / kSub;               // 32-byte chains per round
   constexpr int kPiece = kPerThread / kSub;       // bytes per lane per round
-  // dynamic smem: byte table | multiplier windows | lane windows | per-warp tiles
+  // static smem: byte table; dynamic: multiplier windows | lane windows | per-warp tiles
   constexpr int kMuls = kLaneMul ? 2 : kPackMuls;  // tree levels only without lane tables
-  extern __shared__ __align__(16) uint32_t table[];
-  uint32_t* nib = table + kTableWords;
+  __shared__ __align__(16) uint32_t table[kTableWords];
+  extern __shared__ __align__(16) uint32_t dyn[];
+  uint32_t* nib = dyn;
   uint32_t* lanetab = nib + kMuls * 128;
   uint32_t* stage = lanetab + (kLaneMul ? kLaneTabWords : 0);
   __shared__ uint32_t mconst[kPackMuls];
@@ -168,6 +182,7 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
   }
   __syncthreads();
   const uint32_t* tab = table + lane;
+  const uint32_t lane4 = (uint32_t)lane << 2;
   const uint32_t* n32 = nib;
   const uint32_t* nsub = nib + 128;
   const uint32_t* lvl = nib + 256;           // tree levels, 128 words each
@@ -234,7 +249,7 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
               const int4 v = v4[cc * 2 + h];
               const uint32_t word = w == 0 ? (uint32_t)v.x : w == 1 ? (uint32_t)v.y
                                   : w == 2 ? (uint32_t)v.z : (uint32_t)v.w;
-              q4[cc] = fold_word(tab, q4[cc], word);
+              q4[cc] = fold_word(table, lane4, q4[cc], word);
             }
           }
         }
