@@ -35,6 +35,9 @@ def main():
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--i-ckpt", type=int, default=10)
     ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--modes", default="0",
+                    help="comma list of pec_pack modes to compare (0 auto/bulk, 17-20 the "
+                         "bulk engine on 1/2..1/8 of the SMs, 3 the CRC engine)")
     args = ap.parse_args()
     import torch
     import bench
@@ -48,8 +51,19 @@ def main():
     arena = StateArena(layout, ranks=[0], device=dev, expert_tensors=w.expert_tensors)
     L, E = layout.model.num_moe_layers, layout.model.experts_per_layer
     counters = DeviceTokenCounters(L, E, dev)
+    modes = [int(m) for m in args.modes.split(",")]
+    out = {"workload": w.name, "i_ckpt": args.i_ckpt, "iters": args.iters,
+           "rounds": args.rounds, "modes": {}}
+    for mode in modes:
+        out["modes"][str(mode)] = sweep(args, bench, torch, dev, w, layout, arena, counters,
+                                        PecCheckpointer, mode)
+    print(json.dumps(out if len(modes) > 1 else {**out, **out["modes"][str(modes[0])]},
+                     indent=1))
+
+
+def sweep(args, bench, torch, dev, w, layout, arena, counters, PecCheckpointer, mode):
     ck = PecCheckpointer(layout, arena, None, w.pec, w.strategy, i_ckpt=1, ranks=[0],
-                         counters=counters)
+                         counters=counters, pack_mode=mode)
     eng = ck.engine
     eng.reserve(ck.max_snapshot_bytes(), host_buffers=2)
 
@@ -84,10 +98,8 @@ def main():
         })
         print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
     ck.close()
-    print(json.dumps({"workload": w.name, "snap_bytes": snap_bytes,
-                      "pack_ms_alone": round(pack_alone, 3),
-                      "drain_ms_alone": round(drain_alone, 2), "i_ckpt": args.i_ckpt,
-                      "iters": args.iters, "rounds": args.rounds, "sweep": rows}, indent=1))
+    return {"snap_bytes": snap_bytes, "pack_ms_alone": round(pack_alone, 3),
+            "drain_ms_alone": round(drain_alone, 2), "sweep": rows}
 
 
 if __name__ == "__main__":
