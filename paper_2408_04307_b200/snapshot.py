@@ -54,7 +54,7 @@ from .planner import (
     plan_equal,
 )
 from .selector import select_window
-from .staging import DeviceTable, PlanTemplate, StagingLayout
+from .staging import DeviceTable, PlanTemplate, StagingLayout, drain_cuts, split_table
 from .store import StoreEntry
 from .topology import RankLayout
 
@@ -105,6 +105,10 @@ class DeviceCheckpointEngine(CheckpointEngine):
         self.device = arena.device
         self.ranks = tuple(ranks) if ranks is not None else arena.ranks
         self.pack_mode = pack_mode
+        # split host-planned packs so the drain starts after the first
+        # drain_first bytes (cuts grow 4x: 64 MiB, 256 MiB, 1 GiB, ...)
+        self.pipelined_drain = True
+        self.drain_first = 64 << 20
         self.chunk_log2 = chunk_log2
         self.group = control_group
         # high priority: when the pack and training kernels both have CTAs
@@ -258,8 +262,17 @@ class DeviceCheckpointEngine(CheckpointEngine):
         table = np.concatenate(tables) if tables else np.zeros(0, dtype=D.DESC_DTYPE)
         total = D.plan_chunks(table, self.chunk_log2)
         dt = DeviceTable(table, total, self.device, self.chunk_log2)
+        dt.segments = None
         if self.pack_mode == D.MODE_CRC:
             self._crc_scratch(dt)   # with the table: no allocation at pack time
+        elif self.pipelined_drain and drain_cuts(pos, self.drain_first):
+            # the pack in staging-ordered segments, each drained as soon as it
+            # is packed (begin_snapshot): the drain starts ~20 us into the pack
+            dt.segments = [(DeviceTable(sub, n, self.device, self.chunk_log2), lo,
+                            pos if hi is None else hi)
+                           for sub, n, lo, hi in split_table(
+                               table, self.staging.data_ptr(), drain_cuts(pos, self.drain_first),
+                               self.chunk_log2)]
         entry = (dt, layouts, region, pos)
         if key is not None:
             self._tables[key] = entry
@@ -338,13 +351,25 @@ class DeviceCheckpointEngine(CheckpointEngine):
         start = torch.cuda.Event(enable_timing=True)
         rec.pack_done = torch.cuda.Event(enable_timing=True)
         start.record(ps)
-        self._launch_pack(table, ps)
-        rec.pack_done.record(ps)
+        rec.drain_done = torch.cuda.Event(enable_timing=True)
+        if table.segments is not None:
+            for sub, lo, hi in table.segments:
+                D.pack(sub.tensor, sub.n, sub.total_chunks, sub.chunk_log2, self.pack_mode,
+                       stream=ps)
+                seg_done = torch.cuda.Event()
+                seg_done.record(ps)
+                cs.wait_event(seg_done)
+                with torch.cuda.stream(cs):
+                    self._drain_range(host, lo, min(hi, nbytes))
+            rec.pack_done.record(ps)
+        else:
+            self._launch_pack(table, ps)
+            rec.pack_done.record(ps)
         rec.pack_start = start
         cs.wait_event(rec.pack_done)
-        rec.drain_done = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(cs):
-            self._drain(host, nbytes)
+            if table.segments is None:
+                self._drain(host, nbytes)
             if self.pack_mode == D.MODE_CRC and table.n:
                 rec.entry_crc = torch.empty(table.n, dtype=torch.int32, pin_memory=True)
                 rec.entry_crc.copy_(table.entry_crc[:table.n], non_blocking=True)

@@ -93,6 +93,43 @@ class StagingLayout:
         return table, total
 
 
+def drain_cuts(nbytes: int, first: int = 64 << 20, growth: int = 4) -> List[int]:
+    """Staging offsets at which a snapshot's pack is split so its drain can
+    start early: 64 MiB, 256 MiB, 1 GiB, 4 GiB, ... below ``nbytes``.  The
+    first drain piece starts after ~20 us of pack instead of the whole pack;
+    every later piece is packed long before the host link reaches it."""
+    cuts, c = [], first
+    while c < nbytes:
+        cuts.append(c)
+        c *= growth
+    return cuts
+
+
+def split_table(table: np.ndarray, staging_base: int, cuts: Sequence[int],
+                chunk_log2: int = DEFAULT_CHUNK_LOG2
+                ) -> List[Tuple[np.ndarray, int, int, Optional[int]]]:
+    """Split a pack descriptor table at staging byte offsets ``cuts``:
+    returns [(sub_table, total_chunks, lo, hi)] where sub_table copies exactly the bytes the
+    original copies into staging [lo, hi) (rows crossing a cut are split into
+    two copies; first_chunk re-planned per sub-table).  The segments' ranges
+    tile [0, last cut or end) with the final one open-ended (hi = None)."""
+    r0 = table["dst"].astype(np.int64) - staging_base
+    r1 = r0 + table["nbytes"].astype(np.int64)
+    bounds = [0, *cuts, None]
+    out = []
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        a = np.maximum(r0, lo)
+        b = r1 if hi is None else np.minimum(r1, hi)
+        keep = b > a
+        sub = np.zeros(int(keep.sum()), dtype=DESC_DTYPE)
+        shift = (a - r0)[keep].astype(np.uint64)
+        sub["src"] = table["src"][keep] + shift
+        sub["dst"] = table["dst"][keep] + shift
+        sub["nbytes"] = (b - a)[keep].astype(np.uint64)
+        out.append((sub, plan_chunks(sub, chunk_log2), lo, hi))
+    return out
+
+
 class DeviceTable:
     """A descriptor table resident in device memory, ready for pec_pack."""
 

@@ -30,7 +30,10 @@ def _mutate(arena, step):
         v[:: 97].add_(step + 1)
 
 
-def test_toy_sequential_chain_persists_exact_bytes(dev, tmp_path):
+@pytest.mark.parametrize("drain_first", [None, 100_003])
+def test_toy_sequential_chain_persists_exact_bytes(dev, tmp_path, drain_first):
+    """drain_first=100_003: the pipelined drain splits every pack at odd
+    staging offsets (~8 segments, rows cut mid-copy, unaligned pieces)."""
     import torch
     from paper_2408_04307_b200 import configs
     from paper_2408_04307_b200.arena import StateArena
@@ -41,8 +44,14 @@ def test_toy_sequential_chain_persists_exact_bytes(dev, tmp_path):
     arena = StateArena(layout, [0], dev, w.expert_tensors)
     store = DiskStore(tmp_path)
     ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=5)
+    if drain_first is not None:
+        ck.engine.drain_first = drain_first
     ck.prepare()        # staging, pinned buffers and every phase's table up front
     assert len(ck.engine._tables) == ck.plan().period
+    segs = [t[0].segments for t in ck.engine._tables.values()]
+    assert all((s is None) == (drain_first is None) for s in segs)
+    if drain_first is not None:
+        assert min(len(s) for s in segs) >= 5
     expected = {}
     for it in range(1, 31):
         _mutate(arena, it)  # "optimizer step" of iteration it
