@@ -456,6 +456,7 @@ def run_b200(args):
                          counters=counters, control_group=control, pack_mode=mode,
                          chunk_log2=args.chunk_log2)
     eng = ck.engine
+    eng.pipelined_drain = not args.no_pipelined_drain
     eng.reserve(ck.max_snapshot_bytes(), host_buffers=0)
     k_s = w.pec.k_snapshot
     sel = torch.empty((L, min(k_s, E)), dtype=torch.int32, device=dev)
@@ -782,6 +783,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stall", action="store_true")
+    ap.add_argument("--no-pipelined-drain", action="store_true",
+                    help="drain each snapshot only after its whole pack (A/B of the default)")
     ap.add_argument("--stall-iters", type=int, default=40)
     ap.add_argument("--i-ckpt", type=int, default=10)
     ap.add_argument("--fb-ms", type=float, default=100.0)

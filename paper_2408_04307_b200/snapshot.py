@@ -87,6 +87,7 @@ class _Inflight:
     crc_keys: object = None
     pending: object = None                # device plan: (meta, ready) until the drain is enqueued
     persist_due: object = None            # device plan: persist sets per layer
+    early: object = None                  # device plan: rank -> fixed-prefix bytes drained early
 
 
 class DeviceCheckpointEngine(CheckpointEngine):
@@ -487,6 +488,19 @@ class DeviceCheckpointEngine(CheckpointEngine):
         rec = _Inflight({}, dict(self._dev_region), 0, t_begin=time.perf_counter())
         rec.pack_start, rec.pack_done = t0, t1
         rec.pending = (meta, ready, snap_sel_dev.shape[0], snap_sel_dev.numel())
+        # the fixed-prefix drain (each rank's leading non-expert entries) needs
+        # no size from the GPU: enqueue it now, so the host link is busy while
+        # the size copy lands and the host enqueues the rest
+        rec.early = {r: self.templates[r].fixed_prefix if self.pipelined_drain else 0
+                     for r in self.ranks}
+        if any(rec.early.values()):
+            host = self._ensure_host(buf.buffer_id, self._dev_region_bytes)
+            cs = self.copy_stream
+            cs.wait_event(t1)
+            with torch.cuda.stream(cs):
+                for r in self.ranks:
+                    o = self._dev_region[r]
+                    self._drain_range(host, o, o + rec.early[r])
         self._inflight[buf.buffer_id] = rec
         self._pending_bid = buf.buffer_id
         return buf
@@ -506,6 +520,17 @@ class DeviceCheckpointEngine(CheckpointEngine):
             return False
         ready.synchronize()
         buf = self.buffers.buffers[bid]
+        # the rest of each region's used bytes first (the fixed prefix is on
+        # its way since begin_snapshot_device), the host-side plan after
+        used = {r: int(meta[2 * i + 1]) for i, r in enumerate(self.ranks)}
+        host = self._ensure_host(bid, self._dev_region_bytes)
+        cs = self.copy_stream
+        cs.wait_event(rec.pack_done)
+        rec.drain_done = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(cs):
+            for r in self.ranks:
+                o = self._dev_region[r]
+                self._drain_range(host, o + min(rec.early[r], used[r]), o + used[r])
         head = 2 * len(self.ranks)
         snap_h = meta[head:head + n_snap].view(L, -1).tolist()
         pers_h = meta[head + n_snap:].view(L, -1).tolist()
@@ -513,25 +538,17 @@ class DeviceCheckpointEngine(CheckpointEngine):
         rec.persist_due = {m: frozenset(e for e in pers_h[m] if e >= 0) for m in range(L)}
         assignment = build_phase_assignment(self.layout, due, self.strategy)
         buf.content = assignment
-        layouts, used = {}, {}
-        for i, r in enumerate(self.ranks):
+        layouts = {}
+        for r in self.ranks:
             st = StagingLayout.build(assignment.get(r, ()), self.arena, r)
-            used[r] = int(meta[2 * i + 1])
             if st.nbytes != used[r]:
                 raise RuntimeError(f"device plan of rank {r} ({used[r]} B) disagrees with the "
                                    f"host plan ({st.nbytes} B)")
             layouts[r] = st
         last = self.ranks[-1]
         nbytes = self._dev_region[last] + used[last]
-        host = self._ensure_host(bid, self._dev_region_bytes)
         rec.layouts, rec.nbytes = layouts, nbytes
-        cs = self.copy_stream
-        cs.wait_event(rec.pack_done)
-        rec.drain_done = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(cs):
-            for r in self.ranks:        # each region's used bytes only
-                o = self._dev_region[r]
-                self._drain_range(host, o, o + used[r])
             if self.pack_mode == D.MODE_CRC:
                 # template order per rank; dropped entries carry nbytes 0 (crc 0)
                 total_n = sum(t.n for t in self.templates.values())

@@ -176,6 +176,14 @@ class PlanTemplate:
         self.table = table
         self.n = len(table)
         self.max_bytes = StagingLayout.build(self.ranges, arena, rank).nbytes
+        # the leading non-expert rows are kept for every due set, so their
+        # staged bytes [0, fixed_prefix) are known before the device plan is
+        # (the drain can start on them at once)
+        lead = 0
+        while lead < self.n and table[lead]["layer"] < 0:
+            lead += 1
+        self.fixed_prefix = StagingLayout.build(self.ranges[:lead], arena, rank).nbytes \
+            if lead else 0
         self.tensor = torch.from_numpy(table.view(np.uint8).copy()).view(torch.int64).to(device) \
             if self.n else torch.zeros(4, dtype=torch.int64, device=device)
 
