@@ -412,7 +412,7 @@ def run_reference(args):
                              "components": components},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -757,14 +757,32 @@ def run_b200(args):
             # e2e is bounded by the host link every GPU drains through at once
             e2e["per_gpu"] = round(e2e["value"] / world, 3)
             e2e["frac_of_host_link"] = round(e2e["per_gpu"] / link_conc, 4)
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
 
 
+_RESULT = None  # the real stdout: the JSON line only
+
+
+def _claim_stdout() -> None:
+    """Route fd 1 to stderr for the whole run and keep the original stdout
+    for the one JSON line: libraries that print from C (NCCL's version
+    banner on rank 0 under torchrun) cannot corrupt the contract line."""
+    global _RESULT
+    sys.stdout.flush()
+    _RESULT = os.fdopen(os.dup(1), "w", buffering=1)
+    os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    print(json.dumps(line), file=_RESULT or sys.stdout, flush=True)
+
+
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=8)
