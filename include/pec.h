@@ -144,15 +144,25 @@ int pec_pack_indirect(const pec_copy_desc* descs, int n, uint64_t max_chunks,
 /* ---- pack with fused CRC-32C ------------------ *
  * Replaces: the host CRC of every persisted entry (store.crc32c,
  * store.py:49-70, used for the manifest at store.py:213-216).
- * Same copy as pec_pack (vectorised engine) and, in the same pass over the
- * bytes, entry_crc[i] = CRC-32C of descriptor i's nbytes (== pec_crc32c of
- * the staged entry).  chunk_log2 must be 15; chunk_crc is device scratch of
- * 8 * total_chunks uint32 (one per 4 KiB); entry_crc is device memory of n uint32.
+ * Same copy as pec_pack (TMA bulk ring per warp) and, in the same pass over
+ * the bytes, entry_crc[i] = CRC-32C of descriptor i's nbytes (== pec_crc32c
+ * of the staged entry).  chunk_log2 must be 15; chunk_crc is device scratch
+ * of total_chunks + 1 uint32 (one per 32 KiB chunk, plus the kernel's work
+ * counter); entry_crc is device memory of n uint32.
  * total_chunks_dev (nullable) caps the chunk count from device memory, as in
  * pec_pack_indirect (device-expanded plans). */
 int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
                  const uint64_t* total_chunks_dev, int chunk_log2, uint32_t* chunk_crc,
                  uint32_t* entry_crc, void* stream);
+
+/* CRC-32C of device ranges without copying them: entry_crc[i] = CRC-32C of
+ * [descs[i].src, +nbytes) (dst is ignored).  Same scratch and chunking as
+ * pec_pack_crc.  Used to verify restored entries in device memory before
+ * they are scattered into the state (store.py:267-282 verifies every entry
+ * before load_checkpoint returns any bytes). */
+int pec_crc_device(const pec_copy_desc* descs, int n, uint64_t total_chunks,
+                   const uint64_t* total_chunks_dev, int chunk_log2, uint32_t* chunk_crc,
+                   uint32_t* entry_crc, void* stream);
 
 /* Host helper: fill first_chunk of a HOST table in place and return the
  * total chunk count (negative PEC_E_* on bad input). */

@@ -2,27 +2,41 @@
 //
 // the persist tier checksums each entry
 // (store.crc32c, pkg/src/mocsim/store.py:49-70; the manifest column of
-// store.py:149-164).  Here the pack kernel checksums the bytes it already
-// holds in registers on their way from the state arena to the staging
-// buffer, so the host never reads the payload for CRC and the HBM traffic of
-// the pack is unchanged.
+// store.py:149-164).  Here the pack kernel checksums the bytes on their way
+// from the state arena to the staging buffer, so the host never reads the
+// payload for CRC and the HBM traffic of the pack is unchanged.
 //
-// CRC-32C is linear over GF(2): for the register form R (initial value 0,
-// no final inversion), R(A || B) = R(A) * x^(8|B|) mod P  ^  R(B), and the
-// standard CRC is crc(M) = ~(R(M) ^ ~0 * x^(8|M|) mod P).  So:
-//   pack_crc_kernel   one warp per 4 KiB unit: coalesced 16 B loads, stored
-//                     to staging and through a swizzled per-warp tile so each
-//                     lane then folds ITS contiguous 128 B in four 32-byte
-//                     chains with a byte table kept in shared memory once per
-//                     lane (entry e of lane l at word 32e + l: every lookup of
-//                     a warp hits 32 distinct banks); each lane shifts its
-//                     register to the unit end with its own constant (lane-
-//                     replicated 4-bit-window tables) and a 5-step XOR
-//                     butterfly gives the unit register;
-//   crc_fold_kernel   one thread per 32 KiB chunk joins its 8 unit registers,
-//                     shifts the result by the bytes that follow it in its
-//                     entry and XORs it into the entry's register;
-//   crc_final_kernel  applies the initial value / final inversion per entry.
+// CRC-32C is linear over GF(2).  With the register form R (initial value 0,
+// no final inversion) and little-endian 32-bit words w_0..w_{n-1} of a
+// message, R(M) = XOR_i w_i * x^(32 (n - i)) mod P, R(A || B) =
+// R(A) * x^(8|B|) ^ R(B), and the standard CRC is
+// crc(M) = ~(R(M) ^ ~0 * x^(8|M|) mod P).
+//
+// pack_crc_kernel (one persistent CTA per SM, 8 warps, each warp owns whole
+// 32 KiB chunks, chunk c -> warp c mod #warps):
+//   * each warp streams its chunks as 4 KiB stages through its own ring in
+//     shared memory: lane 0 issues cp.async.bulk global->smem (mbarrier
+//     complete_tx), then cp.async.bulk smem->global into staging — the bytes
+//     never pass through registers on their way to staging;
+//   * the lanes read the stage as 16-byte slots, lane l taking slot
+//     l + 32 j (one 512-byte row per LDS.128: conflict-free), so lane l word
+//     t of row j is message word 128 j + 4 l + t.  Each (lane, t) keeps a
+//     chain S <- S * Y ^ w with Y = x^4096 (its consecutive words are 512 B
+//     apart), over the 64 rows of the chunk;
+//   * S * Y is four byte lookups (slicing-by-4 with tables for Y): tables
+//     live in shared memory replicated 16x, tables 0/1 in banks 0-15 and
+//     2/3 in banks 16-31, and the upper half-warp visits the byte positions
+//     in the order 2,3,0,1 — so every lookup of a warp hits 32 distinct
+//     banks.  A PRMT forms each lookup address (byte of S in bits 8-15, the
+//     lane's bank slot in bits 0-7): 2 instructions per lookup;
+//   * per chunk, lane l joins its chains (x^(32 (4 - t))) and shifts by its
+//     lane constant x^(128 (31 - l)); a XOR butterfly gives R(chunk).
+//   Chunks that are partial (an entry's last) or not 16-byte aligned take a
+//   byte loop per lane instead (at most one per entry for staged plans).
+// crc_fold_kernel  Horner-joins the chunk registers of every entry
+//   (x^(8 * 32 KiB) per chunk, one atomic per thread run).
+// crc_final_kernel applies the last chunk's length, the initial value and
+//   the final inversion per entry.
 // Multiplication mod P (reflected, bit 31 = x^0) is the shift-and-add
 // schoolbook product or, for constants, 8 lookups of 4-bit-window tables;
 // x^(2^k) are precomputed on the host.
@@ -36,23 +50,23 @@
 namespace {
 
 using pecdev::as_stream;
-using pecdev::find_desc;
 using pecdev::launch_status;
 using pecdev::sm_count;
 
 constexpr uint32_t kPoly = 0x82F63B78u;
-constexpr int kCrcThreads = 256;
-constexpr int kCrcLg = 15;                            // 32 KiB chunks
-constexpr int kPerThread = (1 << kCrcLg) / kCrcThreads;  // 128 contiguous bytes
-constexpr int kVecPerThread = kPerThread / 16;        // 8 x 16 B
-constexpr int kTableWords = 256 * 32;                 // lane-replicated byte table
+constexpr int kCrcLg = 15;                      // 32 KiB chunks
+constexpr int kChunk = 1 << kCrcLg;
+constexpr int kStageLg = 12;                    // 4 KiB stages
+constexpr int kStage = 1 << kStageLg;
+constexpr int kStagesPerChunk = kChunk / kStage;
+constexpr int kRowsPerStage = kStage / 512;     // 512-byte rows (32 lanes x 16 B)
+constexpr int kWarps = 8;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kRing = 4;                        // stages per warp
 
-// Constant multipliers are applied through 4-bit windows: mul(a, b) =
-// XOR_p N_a[p][(b >> 4p) & 15] with N_a[p][v] = a * (v << 4p): 8 shared-memory
-// lookups instead of a 32-step schoolbook product (tables built per CTA).
 struct CrcConsts {
   uint32_t x2k[64];         // x^(2^k) mod P
-  uint32_t unit;            // x^(8 * 4096): one 4 KiB unit
+  uint32_t y;               // x^4096: one chain step (512 bytes)
 };
 
 __host__ __device__ __forceinline__ uint32_t gf2_mul(uint32_t a, uint32_t b) {
@@ -65,39 +79,19 @@ __host__ __device__ __forceinline__ uint32_t gf2_mul(uint32_t a, uint32_t b) {
   return p;
 }
 
-__device__ __forceinline__ uint32_t xpow_bytes(const uint32_t* x2k, uint64_t nbytes) {
+__device__ __forceinline__ uint32_t xpow_bits(const uint32_t* x2k, uint64_t nbits) {
   uint32_t acc = 1u << 31;  // 1
-  int k = 3;                // 8 bits per byte
-  while (nbytes) {
-    if (nbytes & 1u) acc = gf2_mul(x2k[k], acc);
-    nbytes >>= 1;
+  int k = 0;
+  while (nbits) {
+    if (nbits & 1u) acc = gf2_mul(x2k[k], acc);
+    nbits >>= 1;
     ++k;
   }
   return acc;
 }
 
 __device__ __forceinline__ uint32_t shift_bytes(const uint32_t* x2k, uint32_t r, uint64_t n) {
-  return n ? gf2_mul(xpow_bytes(x2k, n), r) : r;
-}
-
-// Byte-table lookup at the lane-replicated slot: entry e of lane l is word
-// 32e + l, i.e. byte offset (e << 7) | (l << 2) from the table base, formed by
-// one shift and one LOP3 ((c << 7) & 0x7F80 | lane4).  The table is a static
-// shared array, so its base is an immediate of the LDS (no per-lookup add),
-// and the LOP3 is opaque so the compiler cannot re-associate lane4 into a
-// base register.
-__device__ __forceinline__ uint32_t lut(const uint32_t* table, uint32_t c, uint32_t lane4) {
-  uint32_t off;
-  asm("lop3.b32 %0, %1, 0x7F80, %2, 0xEA;" : "=r"(off) : "r"(c << 7), "r"(lane4));
-  return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(table) + off);
-}
-
-__device__ __forceinline__ uint32_t fold_word(const uint32_t* table, uint32_t lane4, uint32_t c,
-                                              uint32_t w) {
-  c ^= w;
-#pragma unroll
-  for (int b = 0; b < 4; ++b) c = lut(table, c, lane4) ^ (c >> 8);
-  return c;
+  return n ? gf2_mul(xpow_bits(x2k, n << 3), r) : r;
 }
 
 __device__ __forceinline__ uint32_t mul_const(const uint32_t* nib, uint32_t b) {
@@ -107,244 +101,356 @@ __device__ __forceinline__ uint32_t mul_const(const uint32_t* nib, uint32_t b) {
   return r;
 }
 
-// Work unit = one warp x 4 KiB (8 units per 32 KiB chunk).  Warps take
-// units independently (no block barrier on the hot path): unit u of the
-// launch is warp-global index + k * total_warps, so neighbouring warps stream
-// neighbouring 4 KiB and every warp keeps its own loads in flight.
-constexpr int kUnitLog2 = 12;
-constexpr int kUnitsPerChunk = 1 << (kCrcLg - kUnitLog2);
-
-// Multipliers the pack kernel builds 4-bit-window tables for (128 words each):
-// [0] x^(8*32) joins a lane's 32-byte chains, [1] x^(8*S) joins its
-// sub-blocks (S = 4096 / kSub bytes), [2..6] x^(8*P*2^j) are the warp-tree
-// levels (P = 128 / kSub bytes per lane per sub-block).
-constexpr int kPackMuls = 7;
-constexpr int kPackMulWords = kPackMuls * 128;
-constexpr int kLaneTabWords = 8 * 16 * 32;  // per-lane x^(8*P*(31-l)) windows
-
-template <int kThreads, int kSub, bool kLaneMul>
-constexpr int pack_crc_smem() {
-  return ((kLaneMul ? 2 * 128 : kPackMulWords) + (kLaneMul ? kLaneTabWords : 0)) * 4 +
-         (kThreads / 32) * (4096 / kSub);
+// ---- TMA bulk helpers (as in pec_kernels.cu) ------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}"
+      :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;"
+      :: "r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes,
+                                         uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+               :: "l"(gmem), "r"(smem_u32(smem)), "r"(bytes), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// kSub: the 4 KiB unit is transposed through a (4096 / kSub)-byte per-warp
-// tile in kSub rounds (smaller tiles: more CTAs per SM).  kLaneMul: a full
-// unit's lanes shift their registers to the unit end with per-lane constant
-// tables (lane l's window table at word 32 * (16 p + v) + l: conflict-free)
-// and a 5-step XOR butterfly, instead of the 5-level multiply tree.
-template <int kThreads, int kSub, int kMinBlocks, bool kLaneMul>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+// ---- shared-memory layout of pack_crc_kernel (dynamic, bytes) --------------
+// ytab     256 entries x 64 words: entry e, table k, lane group g at word
+//          64 e + 32 (k & 1) + 16 (k >> 1) + g   (64 KiB)
+// lanetab  8 x 16 windows x 32 lanes of x^(128 (31 - l))  (16 KiB)
+// nib      4 x 128 windows of x^(32 (4 - t)), t = 0..3   (2 KiB)
+// t8       standard byte table (slow path)                 (1 KiB)
+// x2k      64 words
+// ring     kWarps x kRing x 4 KiB
+// bars     kWarps x kRing mbarriers
+constexpr int kYtabWords = 256 * 64;
+constexpr int kLaneTabWords = 8 * 16 * 32;
+constexpr int kNibWords = 4 * 128;
+constexpr size_t kSmemBytes = (size_t)(kYtabWords + kLaneTabWords + kNibWords + 256 + 64) * 4 +
+                              (size_t)kWarps * kRing * kStage + (size_t)kWarps * kRing * 8;
+
+// One chain step S * Y ^ w: four table lookups at PRMT-formed byte offsets
+// (byte k of S into bits 8-15, the lane's slot for step s in bits 0-7).
+__device__ __forceinline__ uint32_t ystep(const uint8_t* ytab, uint32_t S, uint32_t w,
+                                          const uint32_t (&slot)[4], const uint32_t (&sel)[4]) {
+  uint32_t a[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const uint32_t off = __byte_perm(S, slot[s], sel[s]);
+    a[s] = *reinterpret_cast<const uint32_t*>(ytab + off);
+  }
+  return a[0] ^ a[1] ^ a[2] ^ a[3] ^ w;
+}
+
+constexpr int kQueue = 4;                       // claimed chunks queued per warp
+
+struct QueueEntry {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t ch;
+  uint32_t len;
+  uint32_t fast;
+};
+
+struct ChunkRef {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint32_t len;
+  bool fast;   // full 32 KiB, src and dst 16-byte aligned
+};
+
+__device__ __forceinline__ ChunkRef chunk_ref(const pec_copy_desc* __restrict__ d, int n,
+                                              uint64_t ch, pecdev::DescCursor& cur) {
+  ChunkRef r;
+  const int i = cur.find(d, n, ch);
+  const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << kCrcLg;
+  const uint64_t nb = __ldg(&d[i].nbytes);
+  r.len = off >= nb ? 0u : (uint32_t)(nb - off < (uint64_t)kChunk ? nb - off : kChunk);
+  r.src = reinterpret_cast<const uint8_t*>(__ldg(&d[i].src) + off);
+  r.dst = reinterpret_cast<uint8_t*>(__ldg(&d[i].dst) + off);
+  r.fast = r.len == (uint32_t)kChunk &&
+           ((reinterpret_cast<uintptr_t>(r.src) | reinterpret_cast<uintptr_t>(r.dst)) & 15u) == 0;
+  return r;
+}
+
+template <bool kStore>
+__global__ void __launch_bounds__(kThreads, 1)
 pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
                 const uint64_t* __restrict__ total_dev, CrcConsts k,
-                uint32_t* __restrict__ unit_raw) {
-  constexpr int kVecSub = kVecPerThread / kSub;   // 16-byte vectors per lane per round
-  constexpr int kChains = 4 / kSub;               // 32-byte chains per round
-  constexpr int kPiece = kPerThread / kSub;       // bytes per lane per round
-  // static smem: byte table; dynamic: multiplier windows | lane windows | per-warp tiles
-  constexpr int kMuls = kLaneMul ? 2 : kPackMuls;  // tree levels only without lane tables
-  __shared__ __align__(16) uint32_t table[kTableWords];
-  extern __shared__ __align__(16) uint32_t dyn[];
-  uint32_t* nib = dyn;
-  uint32_t* lanetab = nib + kMuls * 128;
-  uint32_t* stage = lanetab + (kLaneMul ? kLaneTabWords : 0);
-  __shared__ uint32_t mconst[kPackMuls];
+                uint32_t* __restrict__ chunk_raw) {
+  const uint64_t total_cap = total;       // scratch is sized for the launch bound
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* ytab = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* lanetab = ytab + kYtabWords;
+  uint32_t* nib = lanetab + kLaneTabWords;
+  uint32_t* t8 = nib + kNibWords;
+  uint32_t* x2k = t8 + 256;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(x2k + 64);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)kWarps * kRing * kStage);
+  __shared__ QueueEntry queue[kWarps * kQueue];
   __shared__ uint32_t lconst[32];
+  __shared__ uint32_t base[4][256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
   if (total_dev != nullptr) {
     const uint64_t td = *total_dev;
     total = td < total ? td : total;
   }
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < kMuls) {
-    const uint64_t bytes = tid == 0 ? 32 : tid == 1 ? 4096 / kSub
-                                             : (uint64_t)kPiece << (tid - 2);
-    mconst[tid] = xpow_bytes(k.x2k, bytes);
-  } else if (kLaneMul && tid >= 64 && tid < 96) {
-    const int l = tid - 64;
-    lconst[l] = xpow_bytes(k.x2k, (uint64_t)kPiece * (31 - l));
+  // ---- tables ----------------------------------------------------------------
+  if (tid < 64) x2k[tid] = k.x2k[tid];
+  if (tid == 0) {
+    for (int s = 0; s < kWarps * kRing; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int idx = tid; idx < kTableWords; idx += kThreads) {
-    uint32_t c = (uint32_t)(idx >> 5);
+  for (int idx = tid; idx < 1024; idx += kThreads) {
+    const int tk = idx >> 8, e = idx & 255;
+    base[tk][e] = gf2_mul(k.y, (uint32_t)e << (8 * tk));
+  }
+  {
+    uint32_t c = (uint32_t)tid;
 #pragma unroll
     for (int b = 0; b < 8; ++b) c = (c & 1u) ? (c >> 1) ^ kPoly : c >> 1;
-    table[idx] = c;
+    t8[tid] = c;
   }
   __syncthreads();
-  for (int idx = tid; idx < kMuls * 128; idx += kThreads) {
-    const int m = idx >> 7, p = (idx >> 4) & 7, v = idx & 15;
-    nib[idx] = gf2_mul(mconst[m], (uint32_t)v << (4 * p));
+  if (tid < 32) lconst[tid] = xpow_bits(x2k, 128ull * (31 - tid));
+  for (int idx = tid; idx < kYtabWords; idx += kThreads) {
+    // word 64 e + 32 b + 16 o + g holds table k = b | (o << 1), entry e
+    ytab[idx] = base[((idx >> 5) & 1) | (((idx >> 4) & 1) << 1)][idx >> 6];
   }
-  if (kLaneMul) {
-    for (int idx = tid; idx < kLaneTabWords; idx += kThreads) {
-      const int l = idx & 31, pv = idx >> 5, p = pv >> 4, v = pv & 15;
-      lanetab[idx] = gf2_mul(lconst[l], (uint32_t)v << (4 * p));
-    }
+  for (int idx = tid; idx < kNibWords; idx += kThreads) {
+    const int t = idx >> 7, p = (idx >> 4) & 7, v = idx & 15;
+    nib[idx] = gf2_mul(xpow_bits(x2k, 32ull * (4 - t)), (uint32_t)v << (4 * p));
   }
   __syncthreads();
-  const uint32_t* tab = table + lane;
-  const uint32_t lane4 = (uint32_t)lane << 2;
-  const uint32_t* n32 = nib;
-  const uint32_t* nsub = nib + 128;
-  const uint32_t* lvl = nib + 256;           // tree levels, 128 words each
-  const uint32_t* ltab = lanetab + lane;
-  int4* tile = reinterpret_cast<int4*>(stage) + warp * (256 / kSub);
+  for (int idx = tid; idx < kLaneTabWords; idx += kThreads) {
+    const int l = idx & 31, pv = idx >> 5, p = pv >> 4, v = pv & 15;
+    lanetab[idx] = gf2_mul(lconst[l], (uint32_t)v << (4 * p));
+  }
+  __syncthreads();
 
-  const uint64_t units = total * kUnitsPerChunk;
-  const uint64_t warps_total = (uint64_t)gridDim.x * (kThreads / 32);
-  pecdev::DescCursor cur;
-  for (uint64_t u = (uint64_t)blockIdx.x * (kThreads / 32) + warp; u < units;
-       u += warps_total) {
-    const uint64_t ch = u >> (kCrcLg - kUnitLog2);
-    const int i = cur.find(d, n, ch);
-    const uint64_t nb = __ldg(&d[i].nbytes);
-    const uint64_t off = ((ch - __ldg(&d[i].first_chunk)) << kCrcLg) +
-                         ((u & (kUnitsPerChunk - 1)) << kUnitLog2);
-    const uint64_t span = 1ull << kUnitLog2;
-    const uint64_t len = off >= nb ? 0 : (nb - off < span ? nb - off : span);
-    if (len == 0) {
-      if (lane == 0) unit_raw[u] = 0u;
-      continue;
-    }
-    const uint8_t* s = reinterpret_cast<const uint8_t*>(__ldg(&d[i].src) + off);
-    uint8_t* t = reinterpret_cast<uint8_t*>(__ldg(&d[i].dst) + off);
-    const bool fast = len == span && ((reinterpret_cast<uintptr_t>(s) |
-                                      reinterpret_cast<uintptr_t>(t)) & 15u) == 0;
-    uint32_t c = 0;
-    uint32_t my_len;
-    if (fast) {
-      // coalesced 16 B units (lane + 32k) -> staging, and into a swizzled tile
-      // from which each lane reads back ITS contiguous piece conflict-free
-      // (16-byte slot of unit x: x ^ ((x >> 3) & 7)); 32-byte CRC chains.
-      const int4* vs = reinterpret_cast<const int4*>(s);
-      int4* vt = reinterpret_cast<int4*>(t);
-      int4 r[kVecPerThread];
+  // ---- per-lane lookup geometry ----------------------------------------------
+  // step s: the lower half-warp reads byte s of S from table s, the upper
+  // half byte s ^ 2 from table s ^ 2; table k sits in the 32-word block k & 1
+  // at half k >> 1, so both halves of a warp always hit disjoint banks.
+  const uint32_t h = (uint32_t)lane >> 4, g = (uint32_t)lane & 15u;
+  uint32_t slot[4], sel[4];
 #pragma unroll
-      for (int q = 0; q < kVecPerThread; ++q) r[q] = __ldg(vs + lane + 32 * q);
-#pragma unroll
-      for (int q = 0; q < kVecPerThread; ++q) __stcs(vt + lane + 32 * q, r[q]);
-#pragma unroll
-      for (int sb = 0; sb < kSub; ++sb) {
-#pragma unroll
-        for (int q = 0; q < kVecSub; ++q) {
-          const int x = lane + 32 * q;
-          tile[x ^ ((x >> 3) & 7)] = r[sb * kVecSub + q];
-        }
-        __syncwarp();
-        int4 v4[kVecSub];
-#pragma unroll
-        for (int j = 0; j < kVecSub; ++j) {
-          const int x = lane * kVecSub + j;
-          v4[j] = tile[x ^ ((x >> 3) & 7)];
-        }
-        __syncwarp();  // the tile is rewritten next
-        uint32_t q4[kChains];
-#pragma unroll
-        for (int cc = 0; cc < kChains; ++cc) q4[cc] = 0u;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-#pragma unroll
-            for (int cc = 0; cc < kChains; ++cc) {
-              const int4 v = v4[cc * 2 + h];
-              const uint32_t word = w == 0 ? (uint32_t)v.x : w == 1 ? (uint32_t)v.y
-                                  : w == 2 ? (uint32_t)v.z : (uint32_t)v.w;
-              q4[cc] = fold_word(table, lane4, q4[cc], word);
-            }
-          }
-        }
-        uint32_t cs = q4[0];
-#pragma unroll
-        for (int cc = 1; cc < kChains; ++cc) cs = mul_const(n32, cs) ^ q4[cc];
-        c = sb == 0 ? cs : mul_const(nsub, c) ^ cs;
-      }
-      my_len = kPiece;
-      if (kLaneMul) {
-        // shift to the unit end with this lane's constant, XOR over the warp
-        uint32_t x = 0;
-#pragma unroll
-        for (int p = 0; p < 8; ++p) x ^= ltab[(p * 16 + ((c >> (4 * p)) & 15u)) << 5];
-#pragma unroll
-        for (int j = 16; j >= 1; j >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, j);
-        if (lane == 0) unit_raw[u] = x;
-        continue;
-      }
-    } else {
-      // partial or unaligned unit: bytes, 128 per lane
-      const uint64_t lo = (uint64_t)lane * kPerThread;
-      const uint64_t hi = lo + kPerThread < len ? lo + kPerThread : len;
-      for (uint64_t b = lo; b < hi; ++b) {
-        const uint8_t v = s[b];
-        t[b] = v;
-        c = tab[((c ^ v) & 0xFFu) << 5] ^ (c >> 8);
-      }
-      my_len = hi > lo ? (uint32_t)(hi - lo) : 0u;
-    }
-    // warp tree: lanes hold consecutive pieces; fold right neighbours in
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      const uint32_t oc = __shfl_down_sync(0xffffffffu, c, 1 << j);
-      const uint32_t ol = __shfl_down_sync(0xffffffffu, my_len, 1 << j);
-      if ((lane & ((2 << j) - 1)) == 0) {
-        c = (fast ? mul_const(lvl + j * 128, c) : shift_bytes(k.x2k, c, ol)) ^ oc;
-        my_len += ol;
-      }
-    }
-    if (lane == 0) unit_raw[u] = c;
+  for (int s = 0; s < 4; ++s) {
+    const uint32_t tk = (uint32_t)s ^ (h << 1);
+    slot[s] = ((tk & 1u) << 7) | ((tk >> 1) << 6) | (g << 2);
+    sel[s] = 0x6604u | (tk << 4);  // byte0 <- slot, byte1 <- S.byte[tk], bytes 2-3 <- 0
   }
+  const uint8_t* yb = reinterpret_cast<const uint8_t*>(ytab);
+  const uint32_t* ltab = lanetab + lane;
+
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  uint8_t* my_ring = ring + (size_t)warp * kRing * kStage;
+  uint64_t* my_bars = bars + warp * kRing;
+  QueueEntry* q = queue + warp * kQueue;
+  // chunks are claimed dynamically from a counter (slot `total` of the
+  // scratch, zeroed before the launch): SMs that stream faster take more.
+  // Lane 0 keeps one claim in flight (`res`) so the atomic's latency hides
+  // behind a whole chunk of work.
+  uint32_t* claims = chunk_raw + total_cap;
+  uint32_t res = 0;
+  if (lane == 0) res = atomicAdd(claims, 1u);
+
+  // ---- producer: lane 0 issues, every lane tracks the same (uniform) state ----
+  // It claims chunks, queues them for the consumer (fast ones with their 8
+  // stage loads, slow ones as markers), and keeps at most kRing - 2 loads
+  // ahead of the stage being consumed, so a refilled stage's bulk store was
+  // issued one stage earlier (wait_group.read 1 rarely waits).
+  uint32_t issued = 0, consumed = 0, q_tail = 0, q_head = 0;
+  int p_u = kStagesPerChunk;
+  ChunkRef p_ref = {nullptr, nullptr, 0u, false};
+  bool exhausted = false;
+  pecdev::DescCursor p_cur;
+  auto produce = [&]() {
+    while (!exhausted && issued + 2 <= consumed + kRing) {
+      if (p_u == kStagesPerChunk) {
+        if (q_tail - q_head == (uint32_t)kQueue) return;
+        const uint64_t ch = __shfl_sync(0xffffffffu, res, 0);
+        if (ch >= total) {
+          exhausted = true;
+          return;
+        }
+        if (lane == 0) res = atomicAdd(claims, 1u);
+        p_ref = chunk_ref(d, n, ch, p_cur);
+        if (lane == 0) {
+          QueueEntry& e = q[q_tail % kQueue];
+          e.src = p_ref.src;
+          e.dst = p_ref.dst;
+          e.ch = ch;
+          e.len = p_ref.len;
+          e.fast = p_ref.fast ? 1u : 0u;
+        }
+        ++q_tail;
+        if (!p_ref.fast) continue;
+        p_u = 0;
+      }
+      const int s = (int)(issued % kRing);
+      if (lane == 0) {
+        if (kStore) bulk_wait_read1();   // the store that last read this stage
+        mbar_expect_tx(&my_bars[s], kStage);
+        bulk_g2s(my_ring + (size_t)s * kStage, p_ref.src + ((size_t)p_u << kStageLg), kStage,
+                 &my_bars[s], policy);
+      }
+      ++issued;
+      ++p_u;
+    }
+  };
+
+  // ---- consumer ------------------------------------------------------------------
+#pragma unroll 1
+  for (;;) {
+    produce();
+    if (q_head == q_tail) break;            // exhausted and everything consumed
+    __syncwarp();                           // lane 0's queue entry is visible
+    const QueueEntry& e = q[q_head % kQueue];
+    const uint8_t* src = e.src;
+    uint8_t* dst = e.dst;
+    const uint64_t ch = e.ch;
+    const uint32_t len = e.len;
+    const bool fast = e.fast != 0;
+    ++q_head;
+    uint32_t x = 0;  // this lane's share of R(chunk)
+    if (fast) {
+      uint32_t S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+#pragma unroll 1
+      for (int u = 0; u < kStagesPerChunk; ++u) {
+        const int s = (int)(consumed % kRing);
+        mbar_wait(&my_bars[s], (consumed / kRing) & 1u);
+        const uint8_t* stage = my_ring + (size_t)s * kStage;
+        if (kStore && lane == 0) {
+          bulk_s2g(dst + ((size_t)u << kStageLg), stage, kStage, policy);
+          bulk_commit();
+        }
+        const int4* rows = reinterpret_cast<const int4*>(stage) + lane;
+#pragma unroll
+        for (int j = 0; j < kRowsPerStage; ++j) {
+          const int4 v = rows[32 * j];
+          S0 = ystep(yb, S0, (uint32_t)v.x, slot, sel);
+          S1 = ystep(yb, S1, (uint32_t)v.y, slot, sel);
+          S2 = ystep(yb, S2, (uint32_t)v.z, slot, sel);
+          S3 = ystep(yb, S3, (uint32_t)v.w, slot, sel);
+        }
+        __syncwarp();            // every lane has read the stage
+        ++consumed;
+        produce();               // refill the stage consumed one step earlier
+      }
+      const uint32_t c = mul_const(nib, S0) ^ mul_const(nib + 128, S1) ^
+                         mul_const(nib + 256, S2) ^ mul_const(nib + 384, S3);
+#pragma unroll
+      for (int p = 0; p < 8; ++p) x ^= ltab[(p * 16 + ((c >> (4 * p)) & 15u)) << 5];
+#pragma unroll
+      for (int j = 16; j >= 1; j >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, j);
+    } else if (len > 0) {
+      // partial or unaligned chunk: 1 KiB per lane, byte loop, then a warp
+      // tree joins the pieces (right neighbour's length as the shift)
+      constexpr uint32_t kPiece = kChunk / 32;
+      const uint32_t lo = (uint32_t)lane * kPiece;
+      const uint32_t hi = lo + kPiece < len ? lo + kPiece : len;
+      uint32_t c = 0;
+      for (uint32_t b = lo; b < hi; ++b) {
+        const uint8_t v = src[b];
+        if (kStore) dst[b] = v;
+        c = t8[(c ^ v) & 0xFFu] ^ (c >> 8);
+      }
+      uint32_t my_len = hi > lo ? hi - lo : 0u;
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        const uint32_t oc = __shfl_down_sync(0xffffffffu, c, 1 << j);
+        const uint32_t ol = __shfl_down_sync(0xffffffffu, my_len, 1 << j);
+        if ((lane & ((2 << j) - 1)) == 0) {
+          c = shift_bytes(x2k, c, ol) ^ oc;
+          my_len += ol;
+        }
+      }
+      x = c;
+    }
+    if (lane == 0) chunk_raw[ch] = x;
+  }
+  if (kStore && lane == 0) bulk_wait_all();
 }
 
-template <int kThreads, int kSub, int kMinBlocks, bool kLaneMul>
+template <bool kStore>
 int launch_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
                     const uint64_t* total_chunks_dev, const CrcConsts& consts,
                     uint32_t* chunk_crc, cudaStream_t st) {
-  auto kern = pack_crc_kernel<kThreads, kSub, kMinBlocks, kLaneMul>;
-  constexpr int smem = pack_crc_smem<kThreads, kSub, kLaneMul>();
-  static const int per_sm = [&] {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return 0;
-    int blocks = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kThreads, smem);
-    return blocks < 1 ? 1 : blocks;
-  }();
-  if (per_sm == 0) return PEC_E_CUDA;
-  uint64_t grid = (uint64_t)sm_count() * per_sm;
-  const uint64_t need = (total_chunks * kUnitsPerChunk + kThreads / 32 - 1) / (kThreads / 32);
+  static int ready[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return PEC_E_CUDA;
+  if (!ready[dev]) {
+    if (cudaFuncSetAttribute(pack_crc_kernel<kStore>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kSmemBytes) != cudaSuccess)
+      return PEC_E_CUDA;
+    ready[dev] = 1;
+  }
+  // the chunk-claim counter lives after the chunk registers
+  if (cudaMemsetAsync(chunk_crc + total_chunks, 0, sizeof(uint32_t), st) != cudaSuccess)
+    return PEC_E_CUDA;
+  uint64_t grid = (uint64_t)sm_count();
+  const uint64_t need = (total_chunks + kWarps - 1) / kWarps;
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, kThreads, smem, st>>>(descs, n, total_chunks, total_chunks_dev, consts,
-                                                   chunk_crc);
+  pack_crc_kernel<kStore><<<(unsigned)grid, kThreads, kSmemBytes, st>>>(
+      descs, n, total_chunks, total_chunks_dev, consts, chunk_crc);
   return PEC_OK;
 }
 
 // Chunk registers -> entry accumulators.  Each thread takes a contiguous run
-// of chunks, joins every chunk's (up to 8) unit registers (constant 4 KiB
-// shifts through 4-bit-window tables) and Horner-accumulates consecutive
-// chunks of one entry (constant 32 KiB shift), so an entry receives one
-// atomic per thread run instead of one per chunk (2 GB entries have 64 Ki
-// chunks: same-address atomics would serialise).  A run is flushed shifted
-// by the whole chunks that follow it, x^(8 * 32 KiB * j), a product of up to
-// three 256-entry power tables built per CTA by doubling.  The entry's LAST
-// chunk keeps its register in its own first unit slot (only this thread
-// touches that chunk's slots); crc_final_kernel applies the shift by the
-// last chunk's length once per entry and joins it.
+// of chunks and Horner-accumulates consecutive chunks of one entry (constant
+// 32 KiB shift through 4-bit-window tables), so an entry receives one atomic
+// per thread run instead of one per chunk (2 GB entries have 64 Ki chunks:
+// same-address atomics would serialise).  A run is flushed shifted by the
+// whole chunks that follow it, x^(8 * 32 KiB * j), a product of up to three
+// 256-entry power tables built per CTA by doubling.  The entry's LAST chunk
+// keeps its register in its own slot; crc_final_kernel applies the shift by
+// the last chunk's length once per entry and joins it.
 __global__ void __launch_bounds__(256)
 crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
                 const uint64_t* __restrict__ total_dev, CrcConsts k,
-                uint32_t* __restrict__ unit_raw, uint32_t* __restrict__ entry_raw) {
+                const uint32_t* __restrict__ chunk_raw, uint32_t* __restrict__ entry_raw) {
   __shared__ uint32_t x2k[64];
-  __shared__ uint32_t unib[128];        // windows of x^(8 * 4096)
   __shared__ uint32_t cnib[128];        // windows of x^(8 * 32768)
   __shared__ uint32_t pw[3][256];       // x^(8 * 32K * t * 256^r)
   const int tid = threadIdx.x;
   if (tid < 64) x2k[tid] = k.x2k[tid];
   __syncthreads();
-  if (tid < 128) {
-    const int p = (tid >> 4) & 7, v = tid & 15;
-    unib[tid] = gf2_mul(k.unit, (uint32_t)v << (4 * p));
-  } else if (tid < 131) {
-    const int r = tid - 128;
-    uint32_t b = xpow_bytes(x2k, (uint64_t)(1u << kCrcLg) << (8 * r));
+  if (tid < 3) {
+    const int r = tid;
+    uint32_t b = xpow_bits(x2k, ((uint64_t)kChunk * 8) << (8 * r));
     pw[r][0] = 1u << 31;
     for (int l = 0; l < 8; ++l) {  // pw[r][2^l] = base^(2^l)
       pw[r][1 << l] = b;
@@ -389,31 +495,20 @@ crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
   for (uint64_t ch = c0; ch < c1; ++ch) {
     const int i = cur.find(d, n, ch);
     const uint64_t kk = ch - __ldg(&d[i].first_chunk);
-    const uint64_t off = kk << kCrcLg;
     const uint64_t nb = __ldg(&d[i].nbytes);
-    if (off >= nb) continue;
-    const uint64_t end = off + (1ull << kCrcLg) < nb ? off + (1ull << kCrcLg) : nb;
-    uint32_t acc = unit_raw[ch * kUnitsPerChunk];
-    for (int w = 1; w < kUnitsPerChunk; ++w) {
-      const uint64_t uoff = off + ((uint64_t)w << kUnitLog2);
-      if (uoff >= end) break;
-      const uint64_t ulen = end - uoff < (1ull << kUnitLog2) ? end - uoff : (1ull << kUnitLog2);
-      acc = (ulen == (1ull << kUnitLog2) ? mul_const(unib, acc) : shift_bytes(x2k, acc, ulen))
-            ^ unit_raw[ch * kUnitsPerChunk + w];
-    }
-    const uint64_t chunks = (nb + (1ull << kCrcLg) - 1) >> kCrcLg;
+    if ((kk << kCrcLg) >= nb) continue;
+    const uint64_t chunks = (nb + kChunk - 1) >> kCrcLg;
     if (run_entry >= 0 && i != run_entry) flush();
     if (kk == chunks - 1) {
-      unit_raw[ch * kUnitsPerChunk] = acc;   // R(last chunk), joined in crc_final_kernel
-      flush();                               // this entry's run (if any) ends right before it
-      continue;
+      flush();                      // this entry's run (if any) ends right before it
+      continue;                     // R(last chunk) is joined in crc_final_kernel
     }
     if (run_entry < 0) {
       run_entry = i;
       run = 0;
       run_chunks = chunks;
     }
-    run = mul_const(cnib, run) ^ acc;
+    run = mul_const(cnib, run) ^ chunk_raw[ch];
     run_end = kk + 1;
   }
   flush();
@@ -422,7 +517,7 @@ crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
 // Per entry: R = A * x^(8 * len(last chunk)) ^ R(last chunk), then the
 // initial value / final inversion: crc = ~(R ^ ~0 * x^(8 * nbytes)).
 __global__ void crc_final_kernel(const pec_copy_desc* __restrict__ d, int n, CrcConsts k,
-                                 const uint32_t* __restrict__ unit_raw,
+                                 const uint32_t* __restrict__ chunk_raw,
                                  uint32_t* __restrict__ entry) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint64_t nb = d[i].nbytes;
@@ -430,9 +525,9 @@ __global__ void crc_final_kernel(const pec_copy_desc* __restrict__ d, int n, Crc
       entry[i] = 0u;
       continue;
     }
-    const uint64_t chunks = (nb + (1ull << kCrcLg) - 1) >> kCrcLg;
+    const uint64_t chunks = (nb + kChunk - 1) >> kCrcLg;
     const uint64_t last_len = nb - ((chunks - 1) << kCrcLg);
-    const uint32_t r_last = unit_raw[(d[i].first_chunk + chunks - 1) * kUnitsPerChunk];
+    const uint32_t r_last = chunk_raw[d[i].first_chunk + chunks - 1];
     const uint32_t r = shift_bytes(k.x2k, entry[i], last_len) ^ r_last;
     entry[i] = ~(r ^ shift_bytes(k.x2k, 0xFFFFFFFFu, nb));
   }
@@ -445,27 +540,14 @@ CrcConsts make_consts() {
     k.x2k[i] = p;
     p = gf2_mul(p, p);
   }
-  auto xpow = [&](uint64_t nbytes) {
-    uint32_t acc = 1u << 31;
-    int b = 3;
-    while (nbytes) {
-      if (nbytes & 1u) acc = gf2_mul(k.x2k[b], acc);
-      nbytes >>= 1;
-      ++b;
-    }
-    return acc;
-  };
-  k.unit = xpow(1u << kUnitLog2);
+  k.y = k.x2k[12];        // x^4096
   return k;
 }
 
-}  // namespace
-
-extern "C" {
-
-int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
-                 const uint64_t* total_chunks_dev, int chunk_log2, uint32_t* chunk_crc,
-                 uint32_t* entry_crc, void* stream) {
+template <bool kStore>
+int crc_entries(const pec_copy_desc* descs, int n, uint64_t total_chunks,
+                const uint64_t* total_chunks_dev, int chunk_log2, uint32_t* chunk_crc,
+                uint32_t* entry_crc, void* stream) {
   if (chunk_log2 != kCrcLg || n < 0) return PEC_E_INVAL;
   if (n == 0) return PEC_OK;
   if (descs == nullptr || entry_crc == nullptr || (total_chunks > 0 && chunk_crc == nullptr))
@@ -475,10 +557,8 @@ int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
   if (cudaMemsetAsync(entry_crc, 0, sizeof(uint32_t) * (size_t)n, st) != cudaSuccess)
     return PEC_E_CUDA;
   if (total_chunks > 0) {
-    // measured on B200 (profiles/r1/crc_variants.txt): lane-constant shifts
-    // instead of the multiply tree, 4 KiB tiles, 2 CTAs x 8 warps per SM
-    const int rc = launch_pack_crc<256, 1, 3, true>(descs, n, total_chunks, total_chunks_dev,
-                                                     consts, chunk_crc, st);
+    const int rc = launch_pack_crc<kStore>(descs, n, total_chunks, total_chunks_dev, consts,
+                                           chunk_crc, st);
     if (rc != PEC_OK) return rc;
     uint64_t fold_grid = (total_chunks + 255) / 256;
     if (fold_grid > (uint64_t)sm_count()) fold_grid = (uint64_t)sm_count();  // tables per CTA
@@ -487,6 +567,24 @@ int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
   }
   crc_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(descs, n, consts, chunk_crc, entry_crc);
   return launch_status();
+}
+
+}  // namespace
+
+extern "C" {
+
+int pec_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
+                 const uint64_t* total_chunks_dev, int chunk_log2, uint32_t* chunk_crc,
+                 uint32_t* entry_crc, void* stream) {
+  return crc_entries<true>(descs, n, total_chunks, total_chunks_dev, chunk_log2, chunk_crc,
+                           entry_crc, stream);
+}
+
+int pec_crc_device(const pec_copy_desc* descs, int n, uint64_t total_chunks,
+                   const uint64_t* total_chunks_dev, int chunk_log2, uint32_t* chunk_crc,
+                   uint32_t* entry_crc, void* stream) {
+  return crc_entries<false>(descs, n, total_chunks, total_chunks_dev, chunk_log2, chunk_crc,
+                            entry_crc, stream);
 }
 
 }  // extern "C"

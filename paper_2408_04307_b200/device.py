@@ -34,7 +34,14 @@ TEMPLATE_DTYPE = np.dtype([("src_offset", "<u8"), ("nbytes", "<u8"), ("layer", "
 DEFAULT_CHUNK_LOG2 = 15  # 32 KiB work chunks
 
 MODE_AUTO, MODE_VEC, MODE_BULK = 0, 1, 2
-CRC_UNITS_PER_CHUNK = 8  # pec_pack_crc scratch: one uint32 per 4 KiB of every 32 KiB chunk
+
+
+def crc_scratch_words(total_chunks: int) -> int:
+    """pec_pack_crc / pec_crc_device scratch: one uint32 per 32 KiB chunk plus
+    the kernel's work counter."""
+    return int(total_chunks) + 1
+
+
 MODE_CRC = 3  # engine-level: vectorised pack with fused per-entry CRC-32C (pec_pack_crc)
 
 _lib = None
@@ -69,6 +76,7 @@ def _load():
                                     vp, vp, vp]),
         "pec_pack_indirect": (c_int, [vp, c_int, c_u64, vp, c_int, c_int, vp]),
         "pec_pack_crc": (c_int, [vp, c_int, c_u64, vp, c_int, vp, vp, vp]),
+        "pec_crc_device": (c_int, [vp, c_int, c_u64, vp, c_int, vp, vp, vp]),
         "pec_crc32c": (c_u32, [vp, ctypes.c_size_t, c_u32]),
         "pec_crc32c_combine": (c_u32, [c_u32, c_u32, c_u64]),
         "pec_crc32c_many": (c_int, [vp, vp, vp, c_int, vp, c_int]),
@@ -94,7 +102,7 @@ def exported_symbols():
     return ["pec_abi_version", "pec_strerror", "pec_token_hist", "pec_token_hist_i64",
             "pec_select_sequential",
             "pec_select_load_aware", "pec_pack", "pec_unpack", "pec_plan_chunks",
-            "pec_expand_plan", "pec_pack_indirect", "pec_pack_crc",
+            "pec_expand_plan", "pec_pack_indirect", "pec_pack_crc", "pec_crc_device",
             "pec_crc32c", "pec_crc32c_combine", "pec_crc32c_many", "pec_write_files"]
 
 
@@ -244,23 +252,36 @@ def expand_plan(tmpl_dev, n: int, sel, state_base: int, stage_base: int, out_dev
     _check(rc, "pec_expand_plan")
 
 
-def pack_crc(desc_dev, n: int, total_chunks: int, chunk_crc_dev, entry_crc_dev,
-             chunk_log2: int = DEFAULT_CHUNK_LOG2, stream=None, totals_dev=None) -> None:
-    """pec_pack with the CRC-32C of every entry computed in the same pass
-    (entry_crc_dev [n] int32 device; chunk_crc_dev [8 * total] scratch)."""
+def _crc_call(fn_name: str, desc_dev, n: int, total_chunks: int, chunk_crc_dev, entry_crc_dev,
+              chunk_log2: int, stream, totals_dev) -> None:
     import torch
     if n == 0:
         return
-    if chunk_crc_dev.numel() < max(1, CRC_UNITS_PER_CHUNK * total_chunks) \
+    if chunk_crc_dev.numel() < crc_scratch_words(total_chunks) \
             or entry_crc_dev.numel() < n:
         raise SpecValidationError("crc buffers large enough", "chunk/entry crc buffers too small")
     tdev = _dev_ptr(totals_dev, torch.int64, "totals") if totals_dev is not None else None
-    rc = lib().pec_pack_crc(_dev_ptr(desc_dev, desc_dev.dtype, "descriptor table"), n,
-                            total_chunks, tdev, chunk_log2,
-                            _dev_ptr(chunk_crc_dev, torch.int32, "chunk crc"),
-                            _dev_ptr(entry_crc_dev, torch.int32, "entry crc"),
-                            _stream_handle(stream, desc_dev.device))
-    _check(rc, "pec_pack_crc")
+    rc = getattr(lib(), fn_name)(_dev_ptr(desc_dev, desc_dev.dtype, "descriptor table"), n,
+                                 total_chunks, tdev, chunk_log2,
+                                 _dev_ptr(chunk_crc_dev, torch.int32, "chunk crc"),
+                                 _dev_ptr(entry_crc_dev, torch.int32, "entry crc"),
+                                 _stream_handle(stream, desc_dev.device))
+    _check(rc, fn_name)
+
+
+def pack_crc(desc_dev, n: int, total_chunks: int, chunk_crc_dev, entry_crc_dev,
+             chunk_log2: int = DEFAULT_CHUNK_LOG2, stream=None, totals_dev=None) -> None:
+    """pec_pack with the CRC-32C of every entry computed in the same pass
+    (entry_crc_dev [n] int32 device; chunk_crc_dev [total] scratch)."""
+    _crc_call("pec_pack_crc", desc_dev, n, total_chunks, chunk_crc_dev, entry_crc_dev,
+              chunk_log2, stream, totals_dev)
+
+
+def crc_device(desc_dev, n: int, total_chunks: int, chunk_crc_dev, entry_crc_dev,
+               chunk_log2: int = DEFAULT_CHUNK_LOG2, stream=None, totals_dev=None) -> None:
+    """pec_crc_device: CRC-32C of each descriptor's device source range, no copy."""
+    _crc_call("pec_crc_device", desc_dev, n, total_chunks, chunk_crc_dev, entry_crc_dev,
+              chunk_log2, stream, totals_dev)
 
 
 def pack_indirect(desc_dev, n: int, max_chunks: int, totals_dev,

@@ -57,6 +57,7 @@ class _Piece:
     file_off: int = 0
     entry: Optional[str] = None
     entry_crc: int = 0
+    entry_size: int = 0
     last: bool = False
     host: object = None              # host pieces: pinned tensor + offset
     host_off: int = 0
@@ -162,7 +163,8 @@ def _pieces(engine, plan: RecoveryPlan, wanted, slot_bytes: int):
             for lo in range(e.start, e.stop, step):
                 hi = min(e.stop, lo + step)
                 pieces.append(_Piece(key, lo, hi, "file", path=path, file_off=lo - e.start,
-                                     entry=sk, entry_crc=crc, last=hi == e.stop))
+                                     entry=sk, entry_crc=crc, entry_size=e.stop - e.start,
+                                     last=hi == e.stop))
     return pieces, initial, peers
 
 
@@ -234,10 +236,17 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
     given subset ``keys``).  ``engine`` is a DeviceCheckpointEngine whose
     ``store`` (a DiskStore) holds the storage versions.
 
-    ``verify="device"`` checks every storage entry's CRC-32C on the GPU: the
-    scatter runs as `pec_pack_crc`, which checksums each piece while moving
-    it, and the host only chains the per-piece CRCs; ``"host"`` checksums
-    while reading the files.  A mismatch raises ChecksumMismatchError."""
+    Every storage entry is verified BEFORE any of its bytes reach the state
+    arena (the reference's load_checkpoint verifies every entry before it
+    returns bytes, store.py:267-282): the bytes land in a device slot (or,
+    for an entry larger than a slot, a device buffer of the entry's size),
+    ``verify="device"`` checksums them there with `pec_crc_device` and
+    ``"host"`` while reading the files, and only entries whose CRC-32C
+    matches the manifest are scattered (`pec_unpack`).  A batch is committed
+    after the next batch's files are read, so verification never stalls the
+    file reads.  A mismatch raises ChecksumMismatchError before the entry's
+    unit is touched; ``err.committed_units`` lists the units already
+    restored (from verified bytes) when it was raised."""
     if verify not in ("device", "host"):
         raise ValueError("verify must be 'device' or 'host'")
     import time
@@ -255,6 +264,7 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
         torch.cuda.synchronize(dev)
         rep.wall_s = time.perf_counter() - t_start
         return rep
+    split = {p.entry for p in pieces if p.kind == "file" and not (p.last and p.file_off == 0)}
 
     # batches of pieces, each laid out like a staging buffer (congruent mod 256)
     batches: List[List[Tuple[_Piece, int]]] = []
@@ -274,14 +284,67 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
     ring = _ring(engine, slot_bytes)
     s = stream or torch.cuda.Stream(device=dev)
     s.wait_stream(torch.cuda.current_stream(dev))  # e.g. initial fills / prior wipes
-    running: Dict[str, int] = {}   # entry -> chained CRC of the pieces read so far
+    running: Dict[str, int] = {}   # entry -> chained CRC of the pieces verified so far
+    landing: Dict[str, Tuple[object, int]] = {}   # split entry -> (device buffer, src offset)
+    committed: List[str] = []
     timers = []
-    checks = []                    # (batch, pinned per-piece CRCs) for device verification
-    max_pieces = max(len(b) for b in batches)
-    crc_scratch = [None, None]
     crc_host = torch.empty(len(pieces) if verify == "device" else 1, dtype=torch.int32,
                            pin_memory=True)
     crc_pos = 0
+    crc_scratch: Dict[int, Tuple[object, object]] = {}
+
+    def dev_src(p: _Piece, dslot, off: int) -> int:
+        if p.entry in split:
+            buf, base = landing[p.entry]
+            return buf.data_ptr() + base + p.file_off
+        return dslot.data_ptr() + off
+
+    def commit(rec) -> None:
+        """Verify a batch's storage pieces, then scatter what verified."""
+        batch, slot, dslot, hcrc, ready, crcs, _table = rec
+        if ready is not None:
+            ready.synchronize()
+            crcs = [int(v) for v in hcrc.numpy().view(np.uint32)]
+        rows = []
+        units = []
+        keep = []              # landing buffers stay referenced until their scatter is enqueued
+        try:
+            fi = 0
+            for p, off in batch:
+                if p.kind == "file":
+                    _chain(running, p, crcs[fi])
+                    fi += 1
+                    if p.entry in split:
+                        if p.last:       # the whole entry verified: scatter it at once
+                            buf, base = landing.pop(p.entry)
+                            keep.append(buf)
+                            e0 = p.start - p.file_off
+                            rows.append((buf.data_ptr() + base,
+                                         arena.base_address + arena.slot(p.unit).offset + e0,
+                                         p.stop - e0))
+                            units.append(p.unit)
+                        continue
+                rows.append((dslot.data_ptr() + off,
+                             arena.base_address + arena.slot(p.unit).offset + p.start, p.nbytes))
+                units.append(p.unit)
+        except ChecksumMismatchError as err:
+            err.committed_units = sorted(set(committed))
+            raise
+        table = np.zeros(len(rows), dtype=D.DESC_DTYPE)
+        for i, (a, b, n) in enumerate(rows):
+            table[i] = (a, b, n, 0)
+        nchunks = D.plan_chunks(table, chunk_log2)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(s)
+        if rows:
+            dt = DeviceTable(table, nchunks, dev, chunk_log2)
+            D.unpack(dt.tensor, dt.n, dt.total_chunks, chunk_log2, D.MODE_AUTO, stream=s)
+            timers.append((t0, t1, dt))
+        t1.record(s)
+        ring.free[slot] = t1
+        committed.extend(units)
+
+    pending = None
     with ThreadPoolExecutor(max_workers=io_threads) as pool:
         for bi, batch in enumerate(batches):
             slot = bi % 2
@@ -298,55 +361,62 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
                         rep.memory_bytes += p.nbytes
                     else:
                         rep.storage_bytes += p.nbytes
-            files_or_bytes = [(p, off) for p, off in batch if p.kind in ("file", "bytes")]
-            for i_f, (p, _, _) in enumerate(files):
-                if crcs is not None:
-                    _chain(running, p, crcs[i_f])
-                rep.storage_bytes += p.nbytes
-            table = np.zeros(len(batch), dtype=D.DESC_DTYPE)
+                elif p.kind == "file":
+                    rep.storage_bytes += p.nbytes
             with torch.cuda.stream(s):
-                if files_or_bytes:
-                    end = max(off + p.nbytes for p, off in files_or_bytes)
-                    dslot[:end].copy_(hslot[:end], non_blocking=True)
-                for i, (p, off) in enumerate(batch):
+                for p, off in batch:
+                    if p.kind == "file" and p.entry in split and p.entry not in landing:
+                        # a device buffer for the whole entry, allocated on s (reused in
+                        # stream order once its scatter has run)
+                        lo = arena.slot(p.unit).offset + p.start - p.file_off
+                        buf = torch.empty(p.entry_size + STAGE_ALIGN, dtype=torch.uint8,
+                                          device=dev)
+                        landing[p.entry] = (buf, (lo - buf.data_ptr()) % STAGE_ALIGN)
+                for p, off in batch:
                     if p.kind == "host":
                         dslot[off:off + p.nbytes].copy_(p.host[p.host_off:p.host_off + p.nbytes],
                                                         non_blocking=True)
                         rep.memory_bytes += p.nbytes
-                    table[i]["src"] = dslot.data_ptr() + off
-                    table[i]["dst"] = arena.base_address + arena.slot(p.unit).offset + p.start
-                    table[i]["nbytes"] = p.nbytes
-            nchunks = D.plan_chunks(table, chunk_log2)
-            dt = DeviceTable(table, nchunks, dev, chunk_log2)
-            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            t0.record(s)
+                    elif p.kind == "file" and p.entry in split:
+                        buf, base = landing[p.entry]
+                        o = base + p.file_off
+                        buf[o:o + p.nbytes].copy_(hslot[off:off + p.nbytes], non_blocking=True)
+                    else:
+                        dslot[off:off + p.nbytes].copy_(hslot[off:off + p.nbytes],
+                                                        non_blocking=True)
+            hcrc, ready = None, None
             if verify == "device" and files:
-                # per-slot scratch (reused only after the slot's event), one pinned
-                # CRC array for the whole restore (no pinning inside the loop)
-                need = max(1, D.CRC_UNITS_PER_CHUNK * nchunks)
-                if crc_scratch[slot] is None or crc_scratch[slot][0].numel() < need:
-                    crc_scratch[slot] = (torch.empty(need, dtype=torch.int32, device=dev),
-                                         torch.empty(max(1, max_pieces), dtype=torch.int32,
-                                                     device=dev))
-                scratch, ecrc = crc_scratch[slot]
-                D.pack_crc(dt.tensor, dt.n, dt.total_chunks, scratch, ecrc, chunk_log2, stream=s)
+                table = np.zeros(len(files), dtype=D.DESC_DTYPE)
+                for i, (p, off, _) in enumerate(files):
+                    table[i] = (dev_src(p, dslot, off), 0, p.nbytes, 0)
+                nchunks = D.plan_chunks(table, chunk_log2)
+                dt = DeviceTable(table, nchunks, dev, chunk_log2)
+                need = D.crc_scratch_words(nchunks)
+                sc = crc_scratch.get(slot)
+                if sc is None or sc[0].numel() < need or sc[1].numel() < len(files):
+                    sc = (torch.empty(need, dtype=torch.int32, device=dev),
+                          torch.empty(max(len(files), 1), dtype=torch.int32, device=dev))
+                    crc_scratch[slot] = sc
+                D.crc_device(dt.tensor, dt.n, dt.total_chunks, sc[0], sc[1], chunk_log2, stream=s)
                 hcrc = crc_host[crc_pos:crc_pos + dt.n]
                 crc_pos += dt.n
                 with torch.cuda.stream(s):
-                    hcrc.copy_(ecrc[:dt.n], non_blocking=True)
-                checks.append((batch, hcrc))
+                    hcrc.copy_(sc[1][:dt.n], non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(s)
+                rec_table = dt     # alive until the batch commits (after `ready`)
             else:
-                D.unpack(dt.tensor, dt.n, dt.total_chunks, chunk_log2, D.MODE_AUTO, stream=s)
-            t1.record(s)
-            timers.append((t0, t1, dt))
-            ring.free[slot] = t1
+                rec_table = None
+            rec = (batch, slot, dslot, hcrc, ready, crcs, rec_table)
+            # the previous batch commits now: its verification ran while this
+            # batch's files were read
+            if pending is not None:
+                commit(pending)
+            pending = rec
+        if pending is not None:
+            commit(pending)
     torch.cuda.current_stream(dev).wait_stream(s)
     s.synchronize()
-    for batch, hcrc in checks:            # batches in order: pieces chain in file order
-        vals = hcrc.numpy().view(np.uint32)
-        for i, (p, _) in enumerate(batch):
-            if p.kind == "file":
-                _chain(running, p, int(vals[i]))
     for peer in peers.values():
         if peer is not None:
             peer[0].close()

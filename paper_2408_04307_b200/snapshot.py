@@ -282,7 +282,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
     def _crc_scratch(self, table: DeviceTable) -> None:
         import torch
         if getattr(table, "entry_crc", None) is None:
-            table.chunk_crc = torch.empty(max(1, D.CRC_UNITS_PER_CHUNK * table.total_chunks),
+            table.chunk_crc = torch.empty(D.crc_scratch_words(table.total_chunks),
                                           dtype=torch.int32, device=self.device)
             table.entry_crc = torch.empty(max(1, table.n), dtype=torch.int32, device=self.device)
 
@@ -421,7 +421,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
         t0.record(stream)
         if self.pack_mode == D.MODE_CRC and getattr(self, "_dev_entry_crc_r", None) is None:
             self._dev_chunk_crc_r = {
-                r: torch.empty(max(1, D.CRC_UNITS_PER_CHUNK * t.max_chunks(lg)),
+                r: torch.empty(D.crc_scratch_words(t.max_chunks(lg)),
                                dtype=torch.int32, device=self.device)
                 for r, t in self.templates.items()}
             self._dev_entry_crc_r = {r: torch.empty(max(1, t.n), dtype=torch.int32,

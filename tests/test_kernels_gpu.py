@@ -313,7 +313,7 @@ def test_pack_crc_copies_and_checksums_every_entry(dev, congruent):
         table[i] = (state.data_ptr() + s, staging.data_ptr() + t, n, 0)
     total = D.plan_chunks(table, 15)
     dt = torch.from_numpy(table.view(np.uint8).copy()).view(torch.int64).to(dev)
-    chunk = torch.empty(max(1, D.CRC_UNITS_PER_CHUNK * total), dtype=torch.int32, device=dev)
+    chunk = torch.empty(D.crc_scratch_words(total), dtype=torch.int32, device=dev)
     entry = torch.empty(len(copies), dtype=torch.int32, device=dev)
     D.pack_crc(dt, len(copies), total, chunk, entry)
     torch.cuda.synchronize()
@@ -322,6 +322,34 @@ def test_pack_crc_copies_and_checksums_every_entry(dev, congruent):
     got = entry.cpu().numpy().view(np.uint32)
     for (s, _, n), c in zip(copies, got):
         assert int(c) == O.crc32c(host[s:s + n]), (s, n)
+
+
+def test_crc_device_checksums_without_writing(dev):
+    """pec_crc_device: per-entry CRC-32C of device ranges (aligned multi-chunk,
+    byte-granular, partial chunks, empty) equal to the oracle's, and nothing
+    is written anywhere (dst is ignored)."""
+    import torch
+    from paper_2408_04307_b200 import device as D
+    rng = np.random.default_rng(5)
+    size = 16 << 20
+    state = torch.randint(0, 256, (size,), dtype=torch.uint8, device=dev)
+    before = state.clone()
+    ranges = [(0, 0), (3, 1), (256, 32768), (4096, 3 * 32768 + 7), (17, 100_003)]
+    ranges += [(int(rng.integers(0, size // 2)), int(rng.integers(0, 2 << 20))) for _ in range(12)]
+    table = np.zeros(len(ranges), dtype=D.DESC_DTYPE)
+    for i, (s_, n) in enumerate(ranges):
+        table[i] = (state.data_ptr() + s_, 0, n, 0)
+    total = D.plan_chunks(table, 15)
+    dt = torch.from_numpy(table.view(np.uint8).copy()).view(torch.int64).to(dev)
+    chunk = torch.empty(D.crc_scratch_words(total), dtype=torch.int32, device=dev)
+    entry = torch.empty(len(ranges), dtype=torch.int32, device=dev)
+    D.crc_device(dt, len(ranges), total, chunk, entry)
+    torch.cuda.synchronize()
+    assert torch.equal(state, before)
+    host = state.cpu().numpy()
+    got = entry.cpu().numpy().view(np.uint32)
+    for (s_, n), c in zip(ranges, got):
+        assert int(c) == O.crc32c(host[s_:s_ + n]), (s_, n)
 
 
 def test_pack_crc_very_long_entries_use_every_power_table(dev):
@@ -343,7 +371,7 @@ def test_pack_crc_very_long_entries_use_every_power_table(dev):
         pos += n + 256
     total = D.plan_chunks(table, 15)
     dt = torch.from_numpy(table.view(np.uint8).copy()).view(torch.int64).to(dev)
-    chunk = torch.empty(D.CRC_UNITS_PER_CHUNK * total, dtype=torch.int32, device=dev)
+    chunk = torch.empty(D.crc_scratch_words(total), dtype=torch.int32, device=dev)
     entry = torch.empty(len(lens), dtype=torch.int32, device=dev)
     D.pack_crc(dt, len(lens), total, chunk, entry, 15)
     torch.cuda.synchronize()

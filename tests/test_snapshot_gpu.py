@@ -306,7 +306,7 @@ def test_mixtral_rank_full_size_pack_unpack_bit_exact(dev, engine):
         if engine == "bulk":
             D.pack(dt.tensor, dt.n, dt.total_chunks, lg, D.MODE_BULK)
         else:
-            chunk = torch.empty(D.CRC_UNITS_PER_CHUNK * total, dtype=torch.int32, device=dev)
+            chunk = torch.empty(D.crc_scratch_words(total), dtype=torch.int32, device=dev)
             ecrc = torch.empty(dt.n, dtype=torch.int32, device=dev)
             D.pack_crc(dt.tensor, dt.n, dt.total_chunks, chunk, ecrc, lg)
             # independent check: host SSE4.2 CRC-32C of the smallest, a middle and
@@ -727,7 +727,24 @@ def test_restore_detects_a_flipped_byte(dev, tmp_path, verify):
     data = bytearray(victim.read_bytes())
     data[len(data) // 2] ^= 0x40
     victim.write_bytes(bytes(data))
+    arena.buffer.fill_(0xA5)                    # sentinel: what "untouched" looks like
     with pytest.raises(ChecksumMismatchError) as exc:
         restore(ck.engine, plan, verify=verify, slot_bytes=8 << 20)
     assert exc.value.key == "neo.r0"
+    # verify-before-commit (store.py:267-282): the corrupted entry (split over
+    # several slots here) never reached the arena; units reported as committed
+    # hold verified bytes, every other unit is untouched
+    assert arena.unit_bytes("neo.r0").numel() > (8 << 20)   # the split-entry path
+    now = arena.buffer.cpu().numpy()
+    committed = set(exc.value.committed_units)
+    assert "neo.r0" not in committed
+    for key in plan.decisions:
+        if not arena.has(key):
+            continue
+        sl = arena.slot(key)
+        got = now[sl.offset:sl.offset + sl.size]
+        if key in committed:
+            assert np.array_equal(got, good[sl.offset:sl.offset + sl.size]), key
+        elif plan.decisions[key].source == "storage":
+            assert (got == 0xA5).all(), key
     ck.close()

@@ -51,6 +51,17 @@ case "$recipe" in
         -k regex:"pack_crc|crc_fold|crc_final" -s 3 -c 3 -o $O/prof_crc $CMD > $O/ncu_crc.log 2>&1
     echo ncu=$?
     ;;
+  crc_ab)   # CRC-computing pack vs plain pack (Mixtral rank 0), CRC parity tests, ncu of pack_crc
+    timeout 900 python -m pytest tests -m gpu -x -q -k "crc or restore" 2>&1 | tail -3
+    for e in crc bulk crc; do
+      timeout 600 python bench.py --engine $e --steps 10 --warmup 3 --no-e2e --no-cpu --no-stall \
+        > $O/bench_$e.json 2> $O/bench_$e.err; echo $e=$?; cat $O/bench_$e.json
+    done
+    CMD="python bench.py --engine crc --steps 2 --warmup 3 --no-e2e --no-cpu --no-stall"
+    timeout 1200 ncu --set full --clock-control none --import-source on \
+      -k regex:"pack_crc|crc_fold|crc_final" -s 3 -c 3 -o $O/prof_crc $CMD > $O/ncu_crc.log 2>&1
+    echo ncu=$?
+    ;;
   host_link)   # pinned D2H / push probes
     timeout 300 python tools/d2h_probe.py > $O/d2h_probe.json 2>&1; cat $O/d2h_probe.json
     timeout 300 python tools/d2h_push_probe.py > $O/d2h_push_probe.json 2>&1
