@@ -797,9 +797,10 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="mixtral",
                     choices=["toy", "gpt125m", "gpt350m", "gpt350m_la", "mixtral"])
-    ap.add_argument("--engine", default="bulk", choices=["vec", "bulk", "crc"],
-                    help="pack engine: TMA bulk (default), LDG/STG vector, or vector with "
-                         "fused per-entry CRC-32C")
+    ap.add_argument("--engine", default="crc", choices=["vec", "bulk", "crc"],
+                    help="pack engine: TMA bulk ring with fused per-entry CRC-32C (default; "
+                         "the persist tier then never reads payloads for checksums), plain "
+                         "TMA bulk, or LDG/STG vector")
     ap.add_argument("--chunk-log2", type=int, default=15)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--persist", default="auto", choices=["auto", "none", "shm", "disk"])

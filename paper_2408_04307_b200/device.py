@@ -42,7 +42,7 @@ def crc_scratch_words(total_chunks: int) -> int:
     return int(total_chunks) + 1
 
 
-MODE_CRC = 3  # engine-level: vectorised pack with fused per-entry CRC-32C (pec_pack_crc)
+MODE_CRC = 3  # engine-level: pack with fused per-entry CRC-32C (pec_pack_crc); default with a store
 
 _lib = None
 

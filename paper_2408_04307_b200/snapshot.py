@@ -85,6 +85,7 @@ class _Inflight:
     t_begin: float = 0.0
     entry_crc: object = None              # pinned int32 [n] (MODE_CRC)
     crc_keys: object = None
+    crc_segments: object = None           # pipelined MODE_CRC: [(pinned crcs, rows, nbytes)]
     pending: object = None                # device plan: (meta, ready) until the drain is enqueued
     persist_due: object = None            # device plan: persist sets per layer
     early: object = None                  # device plan: rank -> fixed-prefix bytes drained early
@@ -105,12 +106,21 @@ class DeviceCheckpointEngine(CheckpointEngine):
         self.arena = arena
         self.device = arena.device
         self.ranks = tuple(ranks) if ranks is not None else arena.ranks
+        if pack_mode == D.MODE_AUTO:
+            # with a persist tier, the pack computes every entry's CRC-32C in
+            # the same pass (1.0x the plain pack's HBM rate); the persist
+            # thread then writes files without reading them for checksums
+            pack_mode = D.MODE_CRC if store is not None else D.MODE_BULK
         self.pack_mode = pack_mode
         # split host-planned packs so the drain starts after the first
         # drain_first bytes (cuts grow 4x: 64 MiB, 256 MiB, 1 GiB, ...)
         self.pipelined_drain = True
         self.drain_first = 64 << 20
         self.chunk_log2 = chunk_log2
+        # negative-control hook for tests ONLY: False drops the pack stream's
+        # wait on the compute stream (the snapshot then races the update it
+        # must follow; tests/test_overlap_gpu.py proves the test detects it)
+        self._consistency_wait = True
         self.group = control_group
         # high priority: when the pack and training kernels both have CTAs
         # waiting, the pack (the only training-blocking part) goes first
@@ -264,16 +274,23 @@ class DeviceCheckpointEngine(CheckpointEngine):
         total = D.plan_chunks(table, self.chunk_log2)
         dt = DeviceTable(table, total, self.device, self.chunk_log2)
         dt.segments = None
-        if self.pack_mode == D.MODE_CRC:
-            self._crc_scratch(dt)   # with the table: no allocation at pack time
-        elif self.pipelined_drain and drain_cuts(pos, self.drain_first):
+        if self.pipelined_drain and drain_cuts(pos, self.drain_first):
             # the pack in staging-ordered segments, each drained as soon as it
-            # is packed (begin_snapshot): the drain starts ~20 us into the pack
-            dt.segments = [(DeviceTable(sub, n, self.device, self.chunk_log2), lo,
-                            pos if hi is None else hi)
-                           for sub, n, lo, hi in split_table(
-                               table, self.staging.data_ptr(), drain_cuts(pos, self.drain_first),
-                               self.chunk_log2)]
+            # is packed (begin_snapshot): the drain starts ~20 us into the pack.
+            # CRC mode: per-segment entry CRCs, rows split by a cut are joined
+            # on the host (crc32c_combine)
+            dt.segments = []
+            for sub, n, lo, hi, rows in split_table(
+                    table, self.staging.data_ptr(), drain_cuts(pos, self.drain_first),
+                    self.chunk_log2, with_rows=True):
+                sdt = DeviceTable(sub, n, self.device, self.chunk_log2)
+                sdt.rows = rows
+                sdt.row_bytes = sub["nbytes"].astype(np.int64)
+                if self.pack_mode == D.MODE_CRC:
+                    self._crc_scratch(sdt)   # with the table: no allocation at pack time
+                dt.segments.append((sdt, lo, pos if hi is None else hi))
+        elif self.pack_mode == D.MODE_CRC:
+            self._crc_scratch(dt)
         entry = (dt, layouts, region, pos)
         if key is not None:
             self._tables[key] = entry
@@ -346,7 +363,8 @@ class DeviceCheckpointEngine(CheckpointEngine):
         compute = compute_stream or torch.cuda.current_stream(self.device)
         rec = _Inflight(layouts, region, nbytes, t_begin=time.perf_counter())
         ps, cs = self.pack_stream, self.copy_stream
-        ps.wait_stream(compute)                       # state is consistent here
+        if self._consistency_wait:
+            ps.wait_stream(compute)                   # state is consistent here
         if self._staging_free is not None:
             ps.wait_event(self._staging_free)         # previous drain read staging
         start = torch.cuda.Event(enable_timing=True)
@@ -354,14 +372,21 @@ class DeviceCheckpointEngine(CheckpointEngine):
         start.record(ps)
         rec.drain_done = torch.cuda.Event(enable_timing=True)
         if table.segments is not None:
+            crc_mode = self.pack_mode == D.MODE_CRC
+            if crc_mode:
+                rec.crc_segments = []
+                rec.crc_keys = [e.store_key for r in self.ranks for e in layouts[r].entries]
             for sub, lo, hi in table.segments:
-                D.pack(sub.tensor, sub.n, sub.total_chunks, sub.chunk_log2, self.pack_mode,
-                       stream=ps)
+                self._launch_pack(sub, ps)
                 seg_done = torch.cuda.Event()
                 seg_done.record(ps)
                 cs.wait_event(seg_done)
                 with torch.cuda.stream(cs):
                     self._drain_range(host, lo, min(hi, nbytes))
+                    if crc_mode and sub.n:
+                        pinned = torch.empty(sub.n, dtype=torch.int32, pin_memory=True)
+                        pinned.copy_(sub.entry_crc[:sub.n], non_blocking=True)
+                        rec.crc_segments.append((pinned, sub.rows, sub.row_bytes))
             rec.pack_done.record(ps)
         else:
             self._launch_pack(table, ps)
@@ -371,7 +396,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
         with torch.cuda.stream(cs):
             if table.segments is None:
                 self._drain(host, nbytes)
-            if self.pack_mode == D.MODE_CRC and table.n:
+            if self.pack_mode == D.MODE_CRC and table.n and table.segments is None:
                 rec.entry_crc = torch.empty(table.n, dtype=torch.int32, pin_memory=True)
                 rec.entry_crc.copy_(table.entry_crc[:table.n], non_blocking=True)
                 rec.crc_keys = [e.store_key for r in self.ranks for e in layouts[r].entries]
@@ -466,7 +491,8 @@ class DeviceCheckpointEngine(CheckpointEngine):
         self._retract_meta(buf.buffer_id)
         compute = compute_stream or torch.cuda.current_stream(self.device)
         ps, ms = self.pack_stream, self._meta_stream
-        ps.wait_stream(compute)
+        if self._consistency_wait:
+            ps.wait_stream(compute)
         if self._staging_free is not None:
             ps.wait_event(self._staging_free)
         expanded, t0, t1 = self._expand_and_pack(snap_sel_dev, ps)
@@ -623,7 +649,18 @@ class DeviceCheckpointEngine(CheckpointEngine):
     def device_crcs(self, buf: Buffer):
         """store_key -> CRC-32C computed by the pack (MODE_CRC), else None."""
         rec = self._inflight.get(buf.buffer_id)
-        if rec is None or rec.entry_crc is None:
+        if rec is None:
+            return None
+        if rec.crc_segments is not None:
+            # join the pieces of rows split at drain cuts, in staging order
+            crcs = [None] * len(rec.crc_keys)
+            for pinned, rows, nbytes in rec.crc_segments:
+                vals = pinned.numpy().view(np.uint32)
+                for v, r, n in zip(vals, rows, nbytes):
+                    crcs[r] = int(v) if crcs[r] is None else D.crc32c_combine(crcs[r], int(v),
+                                                                               int(n))
+            return {k: (0 if c is None else c) for k, c in zip(rec.crc_keys, crcs)}
+        if rec.entry_crc is None:
             return None
         vals = rec.entry_crc.numpy().view(np.uint32)
         return {k: int(v) for k, v in zip(rec.crc_keys, vals)}

@@ -106,13 +106,16 @@ def drain_cuts(nbytes: int, first: int = 64 << 20, growth: int = 4) -> List[int]
 
 
 def split_table(table: np.ndarray, staging_base: int, cuts: Sequence[int],
-                chunk_log2: int = DEFAULT_CHUNK_LOG2
+                chunk_log2: int = DEFAULT_CHUNK_LOG2, with_rows: bool = False
                 ) -> List[Tuple[np.ndarray, int, int, Optional[int]]]:
     """Split a pack descriptor table at staging byte offsets ``cuts``:
     returns [(sub_table, total_chunks, lo, hi)] where sub_table copies exactly the bytes the
     original copies into staging [lo, hi) (rows crossing a cut are split into
     two copies; first_chunk re-planned per sub-table).  The segments' ranges
-    tile [0, last cut or end) with the final one open-ended (hi = None)."""
+    tile [0, last cut or end) with the final one open-ended (hi = None).
+    ``with_rows`` appends, per segment, the original row index of every
+    sub-row (a split row's pieces are consecutive bytes of it, in segment
+    order: per-piece CRCs combine into the row's CRC)."""
     r0 = table["dst"].astype(np.int64) - staging_base
     r1 = r0 + table["nbytes"].astype(np.int64)
     bounds = [0, *cuts, None]
@@ -126,7 +129,8 @@ def split_table(table: np.ndarray, staging_base: int, cuts: Sequence[int],
         sub["src"] = table["src"][keep] + shift
         sub["dst"] = table["dst"][keep] + shift
         sub["nbytes"] = (b - a)[keep].astype(np.uint64)
-        out.append((sub, plan_chunks(sub, chunk_log2), lo, hi))
+        seg = (sub, plan_chunks(sub, chunk_log2), lo, hi)
+        out.append(seg + (np.flatnonzero(keep),) if with_rows else seg)
     return out
 
 
