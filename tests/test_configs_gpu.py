@@ -97,7 +97,6 @@ def test_config3_gpt350m_dp8_load_aware_summed_counts_full_shape(dev):
     from paper_2408_04307_b200 import device as D
     from paper_2408_04307_b200.arena import StateArena
     from paper_2408_04307_b200.counting import DeviceTokenCounters
-    from paper_2408_04307_b200.distributed import global_two_tier_select
     from paper_2408_04307_b200.staging import PlanTemplate, StagingLayout
     w = configs.gpt350m_16e_load_aware(k_pec=2)
     layout = w.layout()
@@ -113,9 +112,6 @@ def test_config3_gpt350m_dp8_load_aware_summed_counts_full_shape(dev):
     staging = torch.empty(max(t.max_bytes for t in tmpls) + 512, dtype=torch.uint8, device=dev)
     table = torch.empty(max(t.n for t in tmpls) * 4, dtype=torch.int64, device=dev)
     totals = torch.zeros(2, dtype=torch.int64, device=dev)
-
-    class _Summed:   # the all-reduce, done in-process over the eight ranks' counters
-        counts = None
 
     def select_fn(counts2d, k, pool):
         out = torch.empty((L, k), dtype=torch.int32, device=dev)
@@ -135,8 +131,9 @@ def test_config3_gpt350m_dp8_load_aware_summed_counts_full_shape(dev):
         if it % 2:
             continue
         ss, ps, snap_c, pers_c = O.two_tier_load_aware(snap_c, pers_c, K, K)
-        # global = sum of locals (what dist.all_reduce(SUM) computes), one
-        # selection, selected entries zeroed in every local tier
+        # global = sum of locals (what dist.all_reduce(SUM) computes in
+        # global_two_tier_select), one selection, selected entries zeroed in
+        # every local tier
         glob = torch.stack([c.counts for c in counters]).sum(0)
         snap = select_fn(glob[0], K, None)
         pers = select_fn(glob[1], K, snap)
