@@ -59,6 +59,20 @@ from .store import StoreEntry
 from .topology import RankLayout
 
 
+def _own_control_group():
+    """With several processes, the persist thread's commit (all_gather_object
+    + barrier, distributed.commit_version) must not share a communicator with
+    the training thread's NCCL collectives (the counters' all-reduce): the
+    two threads could order them differently on different ranks.  A
+    dedicated gloo group — created collectively, every rank builds its
+    checkpointer at the same point — carries only the persist protocol.
+    Single process: None."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return None
+    return dist.new_group(backend="gloo")
+
+
 class PersistAborted(RuntimeError):
     """A fault interrupted a persist before its version was published."""
 
@@ -117,6 +131,8 @@ class DeviceCheckpointEngine(CheckpointEngine):
         self.pipelined_drain = True
         self.drain_first = 64 << 20
         self.chunk_log2 = chunk_log2
+        if control_group is None and store is not None:
+            control_group = _own_control_group()
         # negative-control hook for tests ONLY: False drops the pack stream's
         # wait on the compute stream (the snapshot then races the update it
         # must follow; tests/test_overlap_gpu.py proves the test detects it)
@@ -509,11 +525,20 @@ class DeviceCheckpointEngine(CheckpointEngine):
                                                          non_blocking=True)
             meta[head + snap_sel_dev.numel():].copy_(persist_sel_dev.reshape(-1),
                                                      non_blocking=True)
+            # the expanded tables themselves: finalize_pending checks every
+            # kept row's staging offset and length against the host plan
+            tabs = torch.empty(sum(4 * self.templates[r].n for r in self.ranks),
+                               dtype=torch.int64, pin_memory=True)
+            o = 0
+            for r in self.ranks:
+                n4 = 4 * self.templates[r].n
+                tabs[o:o + n4].copy_(self._dev_tables[r][:n4], non_blocking=True)
+                o += n4
         ready = torch.cuda.Event()
         ready.record(ms)
         rec = _Inflight({}, dict(self._dev_region), 0, t_begin=time.perf_counter())
         rec.pack_start, rec.pack_done = t0, t1
-        rec.pending = (meta, ready, snap_sel_dev.shape[0], snap_sel_dev.numel())
+        rec.pending = (meta, ready, snap_sel_dev.shape[0], snap_sel_dev.numel(), tabs)
         # the fixed-prefix drain (each rank's leading non-expert entries) needs
         # no size from the GPU: enqueue it now, so the host link is busy while
         # the size copy lands and the host enqueues the rest
@@ -541,7 +566,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
         if bid is None:
             return True
         rec = self._inflight[bid]
-        meta, ready, L, n_snap = rec.pending
+        meta, ready, L, n_snap, tabs = rec.pending
         if not block and not ready.query():
             return False
         ready.synchronize()
@@ -565,11 +590,21 @@ class DeviceCheckpointEngine(CheckpointEngine):
         assignment = build_phase_assignment(self.layout, due, self.strategy)
         buf.content = assignment
         layouts = {}
+        o = 0
+        stage0 = self.staging.data_ptr()
         for r in self.ranks:
             st = StagingLayout.build(assignment.get(r, ()), self.arena, r)
-            if st.nbytes != used[r]:
-                raise RuntimeError(f"device plan of rank {r} ({used[r]} B) disagrees with the "
-                                   f"host plan ({st.nbytes} B)")
+            n = self.templates[r].n
+            rows = tabs[o:o + 4 * n].numpy().reshape(n, 4).view(np.uint64)
+            o += 4 * n
+            kept = rows[rows[:, 2] > 0]
+            dev_rows = list(zip((kept[:, 1] - np.uint64(stage0 + self._dev_region[r])).tolist(),
+                                kept[:, 2].tolist()))
+            host_rows = [(e.stage_offset, e.nbytes) for e in st.entries]
+            if st.nbytes != used[r] or dev_rows != host_rows:
+                raise RuntimeError(f"device plan of rank {r} ({used[r]} B, {len(dev_rows)} "
+                                   f"rows) disagrees with the host plan ({st.nbytes} B, "
+                                   f"{len(host_rows)} rows)")
             layouts[r] = st
         last = self.ranks[-1]
         nbytes = self._dev_region[last] + used[last]
@@ -880,6 +915,8 @@ class PecCheckpointer:
     def checkpoint(self, iteration: int) -> Buffer:
         c = iteration // self.i_ckpt - 1
         if self.counters is not None:
+            if len(self._cum_at) > 2 * len(self.engine.buffers.buffers) + 8:
+                self._prune_history()
             self._cum_at[iteration] = self._timeline_delivered()
         if self.device_plans:
             return self._checkpoint_device(iteration, c)
@@ -990,6 +1027,39 @@ class PecCheckpointer:
         if self.counters is not None:
             self._reset_counters(expert_restore, restart)
         return RecoveryOutcome(restart, skew, plan, report, expert_restore)
+
+    def _prune_history(self) -> None:
+        """Bound the per-checkpoint history: a counter reset after a fault
+        needs the cumulative delivered tokens only at iterations some expert
+        can be restored to — a buffer still holding a snapshot, or the newest
+        stored version that holds the expert (resolve_recovery's choice,
+        engine.py:231-284) — plus the latest.  Persist sets are needed only
+        for buffers that have not been persisted yet."""
+        bufs = [b for b in self.engine.buffers.buffers if b.version is not None]
+        keep = {b.iteration for b in bufs}
+        if self._cum_at:
+            keep.add(max(self._cum_at))
+        store = self.engine.store
+        if store is not None:
+            want = {f"{t}.L{m}.E{e}" for t in ("ew", "eo")
+                    for m in range(self.layout.model.num_moe_layers)
+                    for e in range(self.layout.model.experts_per_layer)}
+            metas = self.__dict__.setdefault("_meta_cache", {})
+            for v in sorted(store.complete_versions(), reverse=True):
+                if not want:
+                    break
+                if v not in metas:
+                    meta = store.meta(v)
+                    metas[v] = (meta.iteration, {e.unit_key for e in meta.entries.values()})
+                it, units = metas[v]
+                hit = want & units
+                if hit:
+                    keep.add(it)
+                    want -= hit
+        self._cum_at = {k: v for k, v in self._cum_at.items() if k in keep}
+        live = {b.version for b in bufs}
+        for v in [v for v in self.persist_sel if v not in live]:
+            del self.persist_sel[v]
 
     def _reset_counters(self, expert_restore: Dict[Tuple[int, int], int], restart: int) -> None:
         """unsaved(m, e) = tokens delivered in (restored(m, e), restart], from

@@ -11,4 +11,14 @@ from paper_2408_04307_b200 import engine, planner, selector, store, topology  # 
 
 for _name in ("engine", "planner", "selector", "store", "topology"):
     sys.modules[f"mocsim.{_name}"] = getattr(_pkg, _name)
+
+
+def _out_of_scope(*_a, **_k):
+    raise NotImplementedError("the Dynamic-K controller (reference selector.py:103-133) is "
+                              "outside the PEC snapshot path; its tests are deselected")
+
+
+# the reference's test_selector.py imports these at module level; the tests
+# that call them are deselected by tests/test_reference_suite.py
+DynamicKState = dynamic_k_step = _out_of_scope
 __version__ = _pkg.__version__

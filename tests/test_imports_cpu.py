@@ -38,3 +38,28 @@ def test_package_imports_resolve(path):
                 continue
             if not hasattr(m, n):
                 importlib.import_module(f"{mod}.{n}")  # a submodule
+
+
+def test_product_never_imports_the_oracle():
+    """The oracle is test infrastructure: no module of the package (the
+    product path) may import it, statically or lazily, and importing the
+    package (with its native library) must not pull it in."""
+    import subprocess
+    import sys
+    for path in sorted((ROOT / PKG).glob("*.py")):
+        tree = ast.parse(path.read_text())
+        for node in ast.walk(tree):
+            names = []
+            if isinstance(node, ast.Import):
+                names = [a.name for a in node.names]
+            elif isinstance(node, ast.ImportFrom) and node.module and node.level == 0:
+                names = [node.module]
+            for n in names:
+                assert n != "oracle" and not n.startswith("oracle."), (path.name, n)
+        assert "pec_oracle" not in path.read_text(), path.name
+    code = ("import sys, paper_2408_04307_b200 as p; from paper_2408_04307_b200 import device, "
+            "snapshot, restore, store, staging; device.lib(); "
+            "print(sorted(m for m in sys.modules if m == 'oracle' or m.startswith('oracle.')))")
+    res = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    assert res.stdout.strip() == "[]", res.stdout
