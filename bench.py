@@ -5,14 +5,23 @@ One *step* = one PEC checkpoint snapshot of this rank's shard: on-device K_pec
 selection for checkpoint c, then the pack of the rank's planned byte ranges
 (experts' bf16 weights + fp32 master/m/v, its ZeRO-2 non-expert optimizer
 shard, its share of the non-expert weights) from the HBM state arena into the
-HBM staging buffer.  `value` is that with the state already resident in HBM;
-`e2e` adds the copy-engine drain of the staging buffer into a pinned host
-snapshot buffer (the reference's SNAPSHOTTED state: bytes in CPU memory) and
-the host read of the step result, through the package's public API.
+HBM staging buffer, with every entry's CRC-32C computed in the same pass (the
+default engine).  `value` is that with the state already resident in HBM: the
+training-blocking part of a snapshot.  `e2e` is the reference's SNAPSHOTTED
+state (bytes in CPU memory, simulator.py:434-438) through the package's public
+API: router-id H2D + count + select + pack + copy-engine drain into a pinned
+host snapshot buffer + host read, every step.
 
 Workload (default): Mixtral-8x7B-shaped state, K_pec=1, adaptive_pec plan of
 the dp=ep=8 deployment; with N GPUs, ranks 0..N-1 of that plan (weak scaling:
 each GPU holds the same-size ~85 GB rank shard at every N).
+
+Legs (all in one run): device steps (`value`, `roofline`), host-link peaks,
+e2e (>= 5 steps, snapshot tier only), one persist probe, the checkpoint
+cadence the policy derives from this run's measured pack / drain / persist
+rates, then the steady-state training-stall A/B with the persist tier on
+(>= 12 checkpoints per arm, every drain and persist inside the timed window),
+and on rank 0 at N=1 the CPU baseline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 """
@@ -20,6 +29,7 @@ each GPU holds the same-size ~85 GB rank shard at every N).
 from __future__ import annotations
 
 import argparse
+import importlib
 import json
 import os
 import statistics
@@ -125,24 +135,28 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(x, world, device):
+def _reduce(x, world, device, op):
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
     t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=op)
     return float(t.item())
+
+
+def max_over_ranks(x, world, device):
+    import torch.distributed as dist
+    return _reduce(x, world, device, dist.ReduceOp.MAX if world > 1 else None)
+
+
+def min_over_ranks(x, world, device):
+    return -max_over_ranks(-x, world, device)
 
 
 def sum_over_ranks(x, world, device):
-    if world == 1:
-        return x
-    import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return _reduce(x, world, device, dist.ReduceOp.SUM if world > 1 else None)
 
 
 def host_buffers_that_fit(nbytes: int, want: int, frac: float = 0.7) -> int:
@@ -159,47 +173,6 @@ def host_buffers_that_fit(nbytes: int, want: int, frac: float = 0.7) -> int:
     return max(0, min(want, int(frac * avail // (local * max(1, nbytes)))))
 
 
-# ---------------------------------------------------------------------------
-# CPU baseline: the oracle's pack restatement on host cores
-# ---------------------------------------------------------------------------
-
-def cpu_pack_sample(entries, sample_bytes: int, threads: int, min_seconds: float):
-    """Pack a bounded sample of this rank's planned ranges from a
-    host-resident state image with the oracle's threaded numpy restatement:
-    every entry of the plan, each cut to the same fraction of its length
-    (sample_bytes / total; at least 256 B), so the sample keeps the
-    workload's mix of entry sizes and alignments.  Repeat until
-    `min_seconds` of CPU work.  Returns (GB/s of payload, description)."""
-    from oracle import pec_oracle as O
-    entries = [e for e in entries if e.nbytes > 0]
-    total = sum(e.nbytes for e in entries)
-    frac = min(1.0, sample_bytes / max(1, total))
-    copies, src_pos, dst_pos = [], 0, 0
-    for e in entries:
-        n = min(e.nbytes, max(256, int(e.nbytes * frac)))
-        src = src_pos + (e.src_offset % 256)
-        dst = dst_pos + ((src - dst_pos) % 256)
-        copies.append((src, dst, n))
-        src_pos = src + n + 256
-        dst_pos = dst + n
-    state = np.random.default_rng(0).integers(0, 256, size=src_pos + 256, dtype=np.uint8)
-    out = np.empty(dst_pos + 256, dtype=np.uint8)
-    payload = sum(c[2] for c in copies)
-    O.pack_threaded(state, copies, out, threads)  # warm
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        O.pack_threaded(state, copies, out, threads)
-        reps += 1
-        if time.perf_counter() - t0 >= min_seconds:
-            break
-    dt = time.perf_counter() - t0
-    desc = (f"oracle numpy pack of {payload / 1e9:.2f} GB: every one of the rank's "
-            f"{len(copies)} planned entries cut to {100 * frac:.1f} % of its length, "
-            f"x{reps} passes, {threads} threads")
-    return payload * reps / dt / 1e9, desc
-
-
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -211,49 +184,252 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_components(layout, strategy: str, k_pec: int, crc_sample: int = 1 << 20):
-    """The reference's other per-checkpoint CPU costs:
-    two-tier load-aware selection (oracle restatement of the reference's
-    Python sort, selector.py:91-100 / simulator.py:339-354), one checkpoint's
-    range plan (build_phase_assignment, planner.py:263-295) and the
-    reference's byte-at-a-time pure-Python CRC-32C (store.py:49-70,
-    restated in the oracle) on a 1 MiB sample, 1 core."""
-    from oracle import pec_oracle as O
-    from paper_2408_04307_b200 import build_phase_assignment
+# ---------------------------------------------------------------------------
+# The reference's CPU path: its own planner on host cores
+# ---------------------------------------------------------------------------
+
+def load_reference():
+    """The UNMODIFIED reference package `mocsim`: installed into
+    baseline/_ref (pip --target, travels to the GPU box), else imported in
+    place from /root/reference (this container).  (module, where) or
+    (None, why)."""
+    for path, where in ((ROOT / "baseline" / "_ref", "baseline/_ref"),
+                        (Path("/root/reference/pkg/src"), "/root/reference")):
+        if (path / "mocsim" / "__init__.py").exists():
+            sys.path.insert(0, str(path))
+            try:
+                return importlib.import_module("mocsim"), where
+            finally:
+                sys.path.remove(str(path))
+    return None, "mocsim not installed (baseline/_ref missing)"
+
+
+def reference_layout(ref, w):
+    """The workload's layout built by the reference's own topology code from
+    the same spec numbers (reference topology.py:286-356)."""
+    import dataclasses
+    m = ref.ModelSpec(**{f.name: getattr(w.model, f.name) for f in dataclasses.fields(w.model)})
+    p = ref.ParallelSpec(**{f.name: getattr(w.parallel, f.name)
+                           for f in dataclasses.fields(w.parallel)})
+    c = ref.ClusterSpec(**{f.name: getattr(w.cluster, f.name)
+                          for f in dataclasses.fields(w.cluster)})
+    return ref.build_layout(m, p, c)
+
+
+def reference_ranges(ref, w, layout, rank: int):
+    """Rank ``rank``'s ranges of checkpoint 0 from the reference planner:
+    the periodic plan (planner.py:298-353) for sequential selection, the
+    per-checkpoint build_phase_assignment (planner.py:263-295) for a
+    load-aware due set of the same size."""
+    pec = ref.PecConfig(k_pec=w.pec.k_pec, selection=w.pec.selection,
+                        k_snapshot=w.pec.k_snapshot, k_persist=w.pec.k_persist)
+    if w.pec.selection == "load_aware":
+        n = layout.model.experts_per_layer
+        due = {m: ref.select_window(0, m, n, pec.k_snapshot, pec.k_snapshot)
+               for m in range(layout.model.num_moe_layers)}
+        return ref.planner.build_phase_assignment(layout, due, w.strategy).get(rank, ())
+    plan = ref.plan_adaptive(layout, pec) if w.strategy == "adaptive_pec" \
+        else ref.plan_equal(layout, pec)
+    return plan.assignments[0].get(rank, ())
+
+
+def host_copies(layout, ranges, rank: int, cap_bytes: int = 0):
+    """(src, dst, n) copies of a rank's ranges over a host image of the
+    units they read (layout order, 256-byte aligned), packed back to back;
+    ``cap_bytes`` > 0 cuts every range to the same fraction (tests)."""
+    used = {a.key for a in ranges if a.stop > a.start}
+    off, pos = {}, 0
+    for u in layout.units:
+        if u.key in used:
+            off[u.key] = pos
+            pos = (pos + u.size_bytes + 255) // 256 * 256
+    total = sum(a.stop - a.start for a in ranges)
+    frac = 1.0 if not cap_bytes or cap_bytes >= total else cap_bytes / total
+    copies, dst = [], 0
+    for a in ranges:
+        n = a.stop - a.start
+        if n <= 0:
+            continue
+        n = n if frac == 1.0 else max(256, int(n * frac))
+        copies.append((off[a.key] + a.start, dst, n))
+        dst += n
+    return copies, pos, dst
+
+
+def fill_sources(state, copies, threads: int) -> None:
+    """First touch of every source range (a byte pattern), multi-threaded."""
+    from concurrent.futures import ThreadPoolExecutor
+    piece = 64 << 20
+    jobs = [(s + o, min(piece, n - o)) for s, _, n in copies for o in range(0, n, piece)]
+
+    def run(job):
+        s, n = job
+        state[s:s + n] = (s >> 20) & 0xFF
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(run, jobs))
+
+
+def reference_components(ref, layout, w):
+    """The reference's other per-checkpoint CPU costs, its own code as-is:
+    two-tier load-aware selection (select_load_aware per layer and tier,
+    selector.py:91-100 as called by simulator.py:339-354), one
+    build_phase_assignment (planner.py:263-295), one plan_adaptive
+    (planner.py:335-342) and its pure-Python CRC-32C (store.py:49-70) on
+    1 MiB, one core."""
     m = layout.model
-    L, E = m.num_moe_layers, m.experts_per_layer
+    L, E, k = m.num_moe_layers, m.experts_per_layer, w.pec.k_pec
     rng = np.random.default_rng(1)
-    snap = rng.integers(0, 1 << 20, (L, E))
-    pers = snap.copy()
-    t0 = time.perf_counter()
-    reps = 0
-    while time.perf_counter() - t0 < 0.5:
-        O.two_tier_load_aware(snap.copy(), pers.copy(), k_pec, k_pec)
-        reps += 1
-    sel_us = (time.perf_counter() - t0) / reps * 1e6
-    due = {l: frozenset(range(k_pec)) for l in range(L)}
-    t0 = time.perf_counter()
-    reps = 0
-    while time.perf_counter() - t0 < 0.5:
-        build_phase_assignment(layout, due, strategy)
-        reps += 1
-    plan_ms = (time.perf_counter() - t0) / reps * 1e3
-    data = rng.integers(0, 256, crc_sample, dtype=np.uint8).tobytes()
-    t0 = time.perf_counter()
-    O.crc32c_py(data)
-    crc_mbs = crc_sample / (time.perf_counter() - t0) / 1e6
-    return {"select_two_tier_us": round(sel_us, 1), "plan_ms": round(plan_ms, 3),
-            "py_crc32c_MBps_1core": round(crc_mbs, 2),
-            "what": "oracle two-tier load-aware selection [L,E]; host planner "
-                    "build_phase_assignment for one due set; reference-style pure-Python "
-                    "CRC-32C on 1 MiB"}
+    counts = rng.integers(0, 1 << 20, (2, L, E))
+    tiers = []
+    for t in range(2):
+        lc = ref.LoadCounters(L, E)
+        for li in range(L):
+            for e in range(E):
+                lc.unsaved_tokens[(li, e)] = int(counts[t, li, e])
+        tiers.append(lc)
+
+    def timed(fn, budget=0.5):
+        t0, reps = time.perf_counter(), 0
+        while True:
+            fn()
+            reps += 1
+            if time.perf_counter() - t0 >= budget:
+                return (time.perf_counter() - t0) / reps
+
+    def two_tier():
+        for li in range(L):
+            s = ref.select_load_aware(tiers[0], li, k)
+            ref.select_load_aware(tiers[1], li, k, restrict_to=s)
+
+    pec = ref.PecConfig(k_pec=k)
+    due = {li: frozenset(range(k)) for li in range(L)}
+    data = rng.integers(0, 256, 1 << 20, dtype=np.uint8).tobytes()
+    return {"select_two_tier_us": round(timed(two_tier) * 1e6, 1),
+            "build_phase_assignment_ms": round(timed(
+                lambda: ref.planner.build_phase_assignment(layout, due, w.strategy)) * 1e3, 3),
+            "plan_adaptive_ms": round(timed(lambda: ref.plan_adaptive(layout, pec), 1.0) * 1e3, 2),
+            "py_crc32c_MBps_1core": round(len(data) / timed(lambda: ref.crc32c(data), 0.2) / 1e6,
+                                          2),
+            "what": "the reference's own select_load_aware x L layers x 2 tiers, "
+                    "build_phase_assignment, plan_adaptive, crc32c (mocsim, unmodified)"}
+
+
+def cpu_pack_shards(w, n_ranks: int, steps: int, warmup: int, threads: int,
+                    cap_bytes: int = 0, min_seconds: float = 0.0):
+    """Pack ranks 0..n_ranks-1's checkpoint-0 shards — ranges from the
+    reference's own planner — on the host cores, one after another in every
+    step, with the oracle's threaded numpy pack (the reference moves no bytes:
+    it models the snapshot as bytes / bandwidth, simulator.py:57-61).
+    Returns (per-step seconds, payload bytes per step, description, ref,
+    layout)."""
+    from oracle import pec_oracle as O
+    ref, where = load_reference()
+    if ref is not None:
+        layout = reference_layout(ref, w)
+        get = lambda r: reference_ranges(ref, w, layout, r)  # noqa: E731
+        src_of = f"mocsim planner ({where})"
+    else:
+        from paper_2408_04307_b200 import build_phase_assignment, plan_adaptive
+        from paper_2408_04307_b200.selector import select_window
+        layout = w.layout()
+        plan = None if w.pec.selection == "load_aware" else plan_adaptive(layout, w.pec)
+
+        def get(r):
+            if plan is not None:
+                return plan.assignments[0].get(r, ())
+            n = layout.model.experts_per_layer
+            due = {m: select_window(0, m, n, w.pec.k_snapshot, w.pec.k_snapshot)
+                   for m in range(layout.model.num_moe_layers)}
+            return build_phase_assignment(layout, due, w.strategy).get(r, ())
+        src_of = f"this package's planner ({where})"
+    shards = [host_copies(layout, get(r), r, cap_bytes) for r in range(n_ranks)]
+    state = np.empty(max(s[1] for s in shards) + 256, dtype=np.uint8)
+    out = np.empty(max(s[2] for s in shards) + 256, dtype=np.uint8)
+    for copies, _, _ in shards:
+        fill_sources(state, copies, threads)
+    payload = sum(s[2] for s in shards)
+    times = []
+    t_start = time.perf_counter()
+    k = 0
+    while True:
+        t0 = time.perf_counter()
+        for copies, _, _ in shards:
+            O.pack_threaded(state, copies, out, threads)
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            times.append(dt)
+        k += 1
+        if k >= warmup + steps and time.perf_counter() - t_start >= min_seconds:
+            break
+    n_entries = sum(len(s[0]) for s in shards)
+    who = f"ranks 0..{n_ranks - 1}" if n_ranks > 1 else "rank 0"
+    desc = (f"oracle threaded numpy pack of {who}'s full checkpoint-0 shard(s) "
+            f"({payload / 1e9:.2f} GB, {n_entries} entries, ranges from {src_of}) "
+            f"from host-resident state, x{len(times)} timed passes, {threads} threads")
+    if cap_bytes:
+        desc += f" [capped to {cap_bytes / 1e9:.2f} GB per rank]"
+    return times, payload, desc, ref, layout
+
+
+def run_reference(args):
+    rank, local, world = env_rank()
+    if rank != 0:
+        return 0
+    n_ranks = max(1, args.gpus)
+    threads = len(os.sched_getaffinity(0))
+    w, _, _ = build_workload(args, 0)
+    cap = int(args.cpu_sample_gb * 1e9) if args.cpu_sample_gb else 0
+    times, payload, desc, ref, layout = cpu_pack_shards(w, n_ranks, args.steps, args.warmup,
+                                                        threads, cap)
+    value = payload / statistics.mean(times) / 1e9
+    try:
+        comps = reference_components(ref, layout, w) if ref is not None else \
+            {"error": "reference not importable"}
+    except Exception as exc:  # reported, never fatal to the line
+        comps = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(statistics.mean(times) * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": w.name, "plan": w.strategy, "selection": w.pec.selection,
+                       "k_pec": w.pec.k_pec,
+                       "ranks": f"0..{n_ranks - 1} of dp={layout.parallel.dp_degree} "
+                                "(host cores, one after another)",
+                       "parallelism": f"dp{layout.parallel.dp_degree}-"
+                                      f"ep{layout.parallel.ep_degree}",
+                       "bytes_per_step": payload, "same_config": not cap},
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads,
+                             "kind": "port", "sample": desc, "cpu_model": cpu_model(),
+                             "components": comps},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    emit(line)
+    return 0
 
 
 # ---------------------------------------------------------------------------
-# exposed checkpoint stall: synthetic training loop with and without PEC
+# B200 arm
 # ---------------------------------------------------------------------------
 
-def prune_store(store, keep: int = 1) -> None:
+def build_workload(args, rank):
+    from paper_2408_04307_b200 import configs
+    from paper_2408_04307_b200.planner import plan_adaptive, plan_equal
+    w = configs.WORKLOADS[args.workload]()
+    layout = w.layout()
+    if w.pec.selection == "load_aware":
+        plan = None  # assignments are built per checkpoint (on device)
+    elif w.strategy == "adaptive_pec":
+        plan = plan_adaptive(layout, w.pec)
+    else:
+        plan = plan_equal(layout, w.pec)
+    if rank >= layout.n_ranks:
+        raise SystemExit(f"rank {rank} >= dp degree {layout.n_ranks} of {w.name}")
+    return w, layout, plan
+
+
+def prune_store(store, keep: int = 2) -> None:
     """Bench-only retention: drop all but the newest ``keep`` complete
     versions (each is a full rank shard; /dev/shm is host RAM)."""
     if store is None or not hasattr(store, "version_dir"):
@@ -263,15 +439,53 @@ def prune_store(store, keep: int = 1) -> None:
         shutil.rmtree(store.version_dir(v), ignore_errors=True)
 
 
-def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float, rounds: int = 3):
-    """Synthetic per-rank training loop on the compute stream: an F&B proxy
-    (bf16 8192^3 GEMMs, calibrated to ~fb_ms) then an update proxy (one
-    in-place pass over the whole state arena: HBM-bound like a fused Adam
-    step over the rank's ~85 GB shard).  With checkpointing, every i_ckpt-th
-    iteration calls PecCheckpointer.checkpoint after its update (the pack
-    photographs the updated state on the side stream, overlapping the next
-    F&B) and every update first waits for the pending pack.  Returns the
-    device time per iteration with/without and the difference."""
+def measure_host_link(eng, world, dev):
+    """Host-link roofline measured in this run, on the drain's own path (the
+    copy stream, 256 MiB pieces): 1 GiB pinned D2H, best of 5, each rank
+    alone in turn, then all ranks started together (per-trial max over
+    ranks).  With one GPU the two are the same measurement."""
+    import torch
+    n = min(1 << 30, eng.staging.numel(), eng.host[0].numel())
+    eng.host[0][:n].copy_(eng.staging[:n])  # first touch of the pinned pages
+    rank = int(os.environ.get("RANK", 0))
+
+    def d2h_ms():
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(eng.copy_stream)
+        with torch.cuda.stream(eng.copy_stream):
+            eng._drain_range(eng.host[0], 0, n)
+        b.record(eng.copy_stream)
+        b.synchronize()
+        return a.elapsed_time(b)
+
+    alone = 1e30
+    for r in range(world):
+        barrier(world)
+        if r == rank:
+            alone = min(d2h_ms() for _ in range(5))
+    link_alone = n / (alone / 1e3) / 1e9
+    if world == 1:
+        return link_alone, link_alone
+    conc = 1e30
+    for _ in range(5):
+        barrier(world)
+        torch.cuda.synchronize()
+        conc = min(conc, max_over_ranks(d2h_ms(), world, dev))
+    return link_alone, n / (conc / 1e3) / 1e9
+
+
+def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds: int,
+                  world: int, rank: int):
+    """Steady-state training-stall A/B on a synthetic per-rank loop: an F&B
+    proxy (bf16 8192^3 GEMMs, ~fb_ms) then an update proxy (one in-place
+    pass over the whole state arena: HBM-bound like a fused Adam step over the
+    rank's ~85 GB shard).  The checkpointed arm takes ``n_ckpt`` checkpoints,
+    one every ``i_ckpt`` iterations after the update, with the persist tier
+    ON (retention keeps the newest 2 versions), then runs one more interval
+    without a checkpoint, then waits for every drain and persist — all inside
+    the timed window, so a persist tier that cannot keep up shows as stall.
+    The next update always waits for the pending pack.  Arms alternate
+    (A B A B) so drifts hit both; device time per iteration, max over ranks."""
     import torch
     a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
     b = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
@@ -293,9 +507,15 @@ def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float, rounds:
     e1.record()
     e1.synchronize()
     update_ms = e0.elapsed_time(e1)
+    iters = (n_ckpt + 1) * i_ckpt
+    store = ck.engine.store
+    stats = ck.engine.stats
 
-    def run(with_ckpt: bool, base_it: int) -> float:
+    def run(with_ckpt: bool, base_it: int):
+        barrier(world)
         torch.cuda.synchronize()
+        w0 = {k: list(v) for k, v in ck.waits.items()}
+        p0 = len(stats["persist_s"])
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(compute)
         for k in range(1, iters + 1):
@@ -306,121 +526,62 @@ def measure_stall(ck, arena, dev, iters: int, i_ckpt: int, fb_ms: float, rounds:
                 ck.poll()
                 ck.wait_pack(stream=compute)        # the update may not race the pack
             words.add_(1)                           # optimizer step
-            if with_ckpt and it % i_ckpt == 0:
+            if with_ckpt and k % i_ckpt == 0 and k <= n_ckpt * i_ckpt:
                 ck.checkpoint(it)                   # select + plan + pack + drain
+                if rank == 0:
+                    prune_store(store)
+        if with_ckpt:
+            ck.finish()                             # every drain and persist, in the window
         t1.record(compute)
         t1.synchronize()
-        return t0.elapsed_time(t1) / iters
+        waits = {k: [ck.waits[k][0] - w0[k][0], ck.waits[k][1] - w0[k][1]] for k in w0}
+        return t0.elapsed_time(t1) / iters, waits, stats["persist_s"][p0:]
 
+    # checkpoint c = iteration // i_ckpt - 1 walks the plan's phases in order
+    ck.i_ckpt = i_ckpt
     run(False, 0)  # warm
-    n_before = len(ck.engine.stats["pack_ms"])
-    # alternate without / with (A B A B) so slow drifts (clocks, other
-    # tenants of the host) hit both arms alike; each arm = mean of its runs
-    runs_without, runs_with = [], []
+    runs_without, runs_with, waits_all, persists = [], [], [], []
     for r in range(rounds):
-        runs_without.append(run(False, 0))
-        runs_with.append(run(True, 10 ** 6 * (r + 1)))
-        ck.finish()
-        prune_store(ck.engine.store)
-    without, with_ = statistics.mean(runs_without), statistics.mean(runs_with)
-    packs = ck.engine.stats["pack_ms"][n_before:]
-    return {"i_ckpt": i_ckpt, "iters": iters, "rounds": rounds,
-            "checkpoints": rounds * (iters // i_ckpt),
-            "fb_ms": round(n_gemm * gemm_ms, 1), "fb_gemms": n_gemm,
+        runs_without.append(run(False, 0)[0])
+        ms, waits, pers = run(True, i_ckpt * 10 ** 6 * (r + 1))
+        runs_with.append(ms)
+        waits_all.append(waits)
+        persists += pers
+    without = max_over_ranks(statistics.mean(runs_without), world, dev)
+    with_ = max_over_ranks(statistics.mean(runs_with), world, dev)
+    packs = stats["pack_ms"][-rounds * n_ckpt:]
+    wait_sum = {k: [sum(w[k][0] for w in waits_all), sum(w[k][1] for w in waits_all)]
+                for k in waits_all[0]}
+    shard = statistics.mean(stats["snap_bytes"][-rounds * n_ckpt:])
+    return {"i_ckpt": i_ckpt, "checkpoints_per_arm": n_ckpt, "iters_per_arm": iters,
+            "rounds": rounds, "fb_ms": round(n_gemm * gemm_ms, 1), "fb_gemms": n_gemm,
             "update_ms": round(update_ms, 2),
             "iter_ms_without": round(without, 3), "iter_ms_with": round(with_, 3),
             "runs_ms_without": [round(x, 3) for x in runs_without],
             "runs_ms_with": [round(x, 3) for x in runs_with],
             "exposed_ms_per_iter": round(with_ - without, 3),
-            # spread of the baseline runs: differences below it are noise
             "noise_ms_per_iter": round((max(runs_without) - min(runs_without)) / 2, 3),
             "pack_ms_in_loop": round(statistics.mean(packs), 3) if packs else None,
-            "overhead_frac": round((with_ - without) / without, 5)}
-
-
-# ---------------------------------------------------------------------------
-
-def build_workload(args, rank):
-    from paper_2408_04307_b200 import configs
-    from paper_2408_04307_b200.planner import plan_adaptive, plan_equal
-    w = configs.WORKLOADS[args.workload]()
-    layout = w.layout()
-    if w.pec.selection == "load_aware":
-        plan = None  # assignments are built per checkpoint (on device)
-    elif w.strategy == "adaptive_pec":
-        plan = plan_adaptive(layout, w.pec)
-    else:
-        plan = plan_equal(layout, w.pec)
-    if rank >= layout.n_ranks:
-        raise SystemExit(f"rank {rank} >= dp degree {layout.n_ranks} of {w.name}")
-    return w, layout, plan
-
-
-def run_reference(args):
-    rank, local, world = env_rank()
-    if rank != 0:
-        return 0
-    threads = len(os.sched_getaffinity(0))
-    from paper_2408_04307_b200.staging import StagingLayout
-    w, layout, plan = build_workload(args, 0)
-
-    class _Slots:  # arena-less offsets (host-only reference arm)
-        def __init__(self):
-            off, self.o = 0, {}
-            for u in layout.units:
-                if 0 in u.replica_ranks and u.size_bytes:
-                    self.o[u.key] = off
-                    off = (off + u.size_bytes + 255) // 256 * 256
-
-        def slot(self, key):
-            class S:
-                pass
-            s = S()
-            s.offset = self.o[key]
-            return s
-
-    if plan is not None:
-        ranges0 = plan.assignments[0][0]
-    else:  # load-aware: a representative due set of the same size (window c=0)
-        from paper_2408_04307_b200.planner import build_phase_assignment
-        from paper_2408_04307_b200.selector import select_window
-        n = layout.model.experts_per_layer
-        due = {m: select_window(0, m, n, w.pec.k_snapshot, w.pec.k_persist)
-               for m in range(layout.model.num_moe_layers)}
-        ranges0 = build_phase_assignment(layout, due, w.strategy)[0]
-    st = StagingLayout.build(ranges0, _Slots(), 0)
-    sample = min(args.cpu_sample_gb, st.payload_bytes / 1e9)
-    per_step = []
-    for i in range(args.warmup + args.steps):
-        gbs, desc = cpu_pack_sample(st.entries, int(sample * 1e9), threads, 0.0)
-        if i >= args.warmup:
-            per_step.append(gbs)
-    value = statistics.mean(per_step)
-    try:
-        components = cpu_components(layout, w.strategy, w.pec.k_pec)
-    except Exception as exc:  # reported, never fatal to the line
-        components = {"error": f"{type(exc).__name__}: {exc}"[:200]}
-    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(sample * 1e9 / (value * 1e9) * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": w.name, "plan": w.strategy, "selection": w.pec.selection,
-                       "k_pec": w.pec.k_pec, "ranks": f"0 of dp={layout.n_ranks} (host cores)",
-                       "parallelism": f"dp{layout.n_ranks}-ep{layout.parallel.ep_degree}",
-                       "sample_gb": round(sample, 3)},
-            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads,
-                             "kind": "port", "sample": desc, "cpu_model": cpu_model(),
-                             "components": components},
-            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    emit(line)
-    return 0
+            "overhead_frac": round((with_ - without) / without, 5),
+            "host_waits": {"snapshot_drain": {"count": wait_sum["snap"][0],
+                                              "s": round(wait_sum["snap"][1], 3)},
+                           "buffer_for_persist": {"count": wait_sum["buffer"][0],
+                                                  "s": round(wait_sum["buffer"][1], 3)},
+                           "what": "host time at checkpoints waiting for the previous drain / "
+                                   "for a persist to free a buffer (NoFreeBufferError, "
+                                   "simulator.py:413-422), summed over the checkpointed arms"},
+            "persist_in_window": {"versions": len(persists),
+                                  "s_mean": round(statistics.mean(persists), 3) if persists
+                                  else None,
+                                  "GBps": round(shard / statistics.mean(persists) / 1e9, 2)
+                                  if persists else None},
+            "window": "every drain and persist of the arm completes inside the timed window"}
 
 
 def run_b200(args):
     import shutil
     import tempfile
+    from dataclasses import replace
     import torch
     rank, local, world = dist_init(args.gpus)
     torch.cuda.set_device(local)
@@ -428,8 +589,8 @@ def run_b200(args):
     from paper_2408_04307_b200 import device as D
     from paper_2408_04307_b200.arena import StateArena
     from paper_2408_04307_b200.counting import DeviceTokenCounters
+    from paper_2408_04307_b200.policy import b200_cadence, b200_configure, drain_bandwidth
     from paper_2408_04307_b200.snapshot import PecCheckpointer
-    from paper_2408_04307_b200.staging import StagingLayout
     from paper_2408_04307_b200.store import DiskStore
 
     w, layout, plan = build_workload(args, rank)
@@ -441,22 +602,23 @@ def run_b200(args):
     routed = w.tokens_per_rank * top_k
     counters = DeviceTokenCounters(L, E, dev, DeviceTokenCounters.capacity_for(
         w.capacity_factor, [routed] * L, E))
-    persist = args.persist if args.persist != "auto" else ("shm" if world == 1 else "none")
-    store_root = None
+    persist = args.persist if args.persist != "auto" else "shm"
     store = None
+    store_root = None
     if persist != "none":
+        # one store root for all ranks (multi-writer commit, distributed.py)
         base = "/dev/shm" if persist == "shm" else tempfile.gettempdir()
-        store_root = tempfile.mkdtemp(prefix="pec_bench_", dir=base)
+        root = [tempfile.mkdtemp(prefix="pec_bench_", dir=base) if rank == 0 else None]
+        if world > 1:
+            import torch.distributed as dist
+            dist.broadcast_object_list(root, src=0)
+        store_root = root[0]
         store = DiskStore(store_root, io_threads=len(os.sched_getaffinity(0)),
                           direct_io=args.direct_io)
-    control = None
-    if world > 1 and store is not None:
-        import torch.distributed as dist
-        control = dist.new_group(backend="gloo")
     mode = {"vec": D.MODE_VEC, "bulk": D.MODE_BULK, "crc": D.MODE_CRC}[args.engine]
+    # the persist protocol gets its own gloo group (created collectively inside)
     ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=1, ranks=[rank],
-                         counters=counters, control_group=control, pack_mode=mode,
-                         chunk_log2=args.chunk_log2)
+                         counters=counters, pack_mode=mode, chunk_log2=args.chunk_log2)
     eng = ck.engine
     eng.pipelined_drain = not args.no_pipelined_drain
     eng.reserve(ck.max_snapshot_bytes(), host_buffers=0)
@@ -467,11 +629,7 @@ def run_b200(args):
     ids_step = torch.randint(0, E, (L, routed), dtype=torch.int32, device=dev,
                              generator=torch.Generator(device=dev).manual_seed(1234 + rank))
     pt = getattr(eng, "template", None)
-    la_bytes = None
-    if plan is None:
-        # payload of the load-aware steps: measured from the host mirror of
-        # each step's selection after the timed region
-        la_bytes = []
+    la_sel = [] if plan is None else None
 
     def step(c):
         """One checkpoint's device work; returns (t0, t1, bytes or None).
@@ -484,9 +642,9 @@ def run_b200(args):
             return eng.pack_only(plan.assignments[p], plan_key=("phase", p), stream=stream)
         with torch.cuda.stream(stream):
             counters.add_iteration(ids_step, stream=stream)
-            snap_d, pers_d = counters.select(k_s, w.pec.k_persist, stream=stream)
+            snap_d, _ = counters.select(k_s, w.pec.k_persist, stream=stream)
         a, b = eng.pack_only_device(snap_d, stream=stream)
-        la_bytes.append(snap_d)
+        la_sel.append(snap_d)
         return a, b, None
 
     if plan is not None:
@@ -528,187 +686,176 @@ def run_b200(args):
     pack_ms = [a.elapsed_time(b) for a, b in evs]
     if plan is None:
         # bytes of each load-aware step from the host mirror of its selection
-        sels = la_bytes[-args.steps:]
         moved = 0
-        for sd in sels:
+        for sd in la_sel[-args.steps:]:
             h = sd.cpu().tolist()
             due = {m: frozenset(x for x in h[m] if x >= 0) for m in range(L)}
             moved += sum(a.stop - a.start for a in pt.select(due))
     max_ms = max_over_ranks(elapsed_ms, world, dev)
     total_moved = sum_over_ranks(moved, world, dev)
     value = total_moved / (max_ms / 1e3) / 1e9
-
     hbm_peak, peak_kind = measured_peaks()
     avg_pack_ms = statistics.mean(pack_ms)
-    achieved = 2 * (moved / args.steps) / (avg_pack_ms / 1e3) / 1e9
+    pack_bw = (moved / args.steps) / (avg_pack_ms / 1e3)          # payload B/s
+    achieved = 2 * pack_bw / 1e9
     traffic = None
     tp = ROOT / "profiles" / "pack_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(w.name)
+            t = json.loads(tp.read_text()).get(w.name)
+            traffic = t.get(args.engine) if isinstance(t, dict) else t
         except Exception:
             traffic = None
 
-    # ---- e2e through the public API: router ids H2D -> count -> select ->
-    #      pack -> drain into pinned host memory (SNAPSHOTTED) -> host read;
-    #      the persist of each version runs behind on the persist thread
-    e2e = None
-    persist_info = None
-    pin_s = 0.0
-    if not (args.no_e2e and args.no_stall):
-        # pin the host snapshot buffers once, before any timing (pinning runs
-        # at ~4-5 GB/s; a training job does this at start-up): 3 with a
-        # persist tier, 2 without (buffers then recycle through RECOVERY)
-        tpin = time.perf_counter()
-        pin_error = None
-        want = 3 if store is not None else 2
-        # never pin more than ~70 % of the node's available RAM (all local
-        # ranks pin at once); every rank uses the node-wide minimum
-        fit = host_buffers_that_fit(eng.staging.numel(), want)
-        n_host = int(-max_over_ranks(-float(fit), world, dev))
-        if n_host < want:
-            print(f"bench: host RAM fits {n_host} of {want} pinned snapshot buffers per rank",
-                  file=sys.stderr)
-        # pinned buffers each leg cycles through (an unpinned one would be
-        # allocated inside a timed region): the stall loop needs RECOVERY +
-        # PERSISTING + SNAPSHOTTING with a persist tier (2 without); the e2e
-        # leg holds the persist tier, so its warm step plus every timed step
-        # need their own buffer with one (buffers recycle without)
-        if n_host < (3 if store is not None else 2):
-            args.no_stall = True
-        warm_e2e = n_host >= 2
-        if store is not None:
-            e2e_cap = n_host - 1 if warm_e2e else 1
-        else:
-            e2e_cap = 2 if warm_e2e else 1
-        args.e2e_steps = max(1, min(args.e2e_steps, e2e_cap))
-        if n_host < 1:
-            pin_error = "host RAM too small for one pinned snapshot buffer per local rank"
-        else:
-            try:
-                eng.reserve(eng.staging.numel(), host_buffers=n_host)
-            except (RuntimeError, MemoryError, OSError) as exc:  # e.g. pinning refused
-                pin_error = f"{type(exc).__name__}: {exc}"[:200]
-        pin_s = time.perf_counter() - tpin
-        if max_over_ranks(1.0 if pin_error else 0.0, world, dev) > 0:
-            # every rank skips the host-buffer legs together (no stranded collectives)
-            print(f"bench: pinned host buffers unavailable ({pin_error}); "
-                  "skipping e2e and stall legs", file=sys.stderr)
-            args.no_e2e = args.no_stall = True
+    # ---- host buffers: pinned once, before any host-side timing -------------
+    tpin = time.perf_counter()
+    fit = host_buffers_that_fit(eng.staging.numel(), 3)
+    n_host = int(min_over_ranks(float(fit), world, dev))    # node-wide minimum
+    pin_error = None
+    if n_host < 2:
+        pin_error = f"host RAM fits {n_host} pinned snapshot buffers per rank (need >= 2)"
+    else:
+        try:
+            eng.reserve(eng.staging.numel(), host_buffers=n_host)
+            for hb in eng.host:                    # first D2H into fresh pages runs slow
+                if hb is not None:
+                    m_ = min(hb.numel(), eng.staging.numel())
+                    hb[:m_].copy_(eng.staging[:m_])
+        except (RuntimeError, MemoryError, OSError) as exc:  # e.g. pinning refused
+            pin_error = f"{type(exc).__name__}: {exc}"[:200]
+    pin_s = time.perf_counter() - tpin
+    if max_over_ranks(1.0 if pin_error else 0.0, world, dev) > 0:
+        print(f"bench: pinned host buffers unavailable ({pin_error}); skipping the host legs",
+              file=sys.stderr)
+        args.no_e2e = args.no_stall = True
+    if n_host < 3:
+        args.no_stall = True      # the steady state needs RECOVERY + PERSISTING + SNAPSHOTTING
+
     link_alone = link_conc = None
+    e2e = host_link = persist_info = cadence = stall = None
     if not args.no_e2e:
-        # host-link roofline measured in this run (1 GiB pinned D2H, best of 3,
-        # after the buffers' first touch): each rank alone in turn, then all
-        # N ranks at once (max over ranks)
-        n_ = min(1 << 30, eng.staging.numel(), eng.host[0].numel())
-        eng.host[0][:n_].copy_(eng.staging[:n_])  # first touch of the pinned pages
+        link_alone, link_conc = measure_host_link(eng, world, dev)
 
-        def d2h_ms():
-            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a_.record(eng.copy_stream)
-            with torch.cuda.stream(eng.copy_stream):
-                eng.host[0][:n_].copy_(eng.staging[:n_], non_blocking=True)
-            b_.record(eng.copy_stream)
-            b_.synchronize()
-            return a_.elapsed_time(b_)
-
-        alone = 1e30
-        for r_ in range(world):
-            barrier(world)
-            if r_ == rank:
-                alone = min(d2h_ms() for _ in range(3))
-        barrier(world)
-        conc = 1e30
-        for _ in range(3):
-            barrier(world)
-            torch.cuda.synchronize()
-            conc = min(conc, max_over_ranks(d2h_ms(), world, dev))
-        link_alone = n_ / (alone / 1e3) / 1e9
-        link_conc = n_ / (conc / 1e3) / 1e9
-    if not args.no_e2e:
-        e2e_steps = max(1, min(args.e2e_steps, 2))  # <= 2 so no buffer waits on persist
+        # ---- e2e through the public API (snapshot tier only) ------------------
+        ck.set_persist(False)
+        n_e2e = max(5, args.e2e_steps)
         rng = np.random.default_rng(1234 + rank)
-        ids_host = [torch.from_numpy(rng.integers(0, E, size=(L, routed), dtype=np.int32)).pin_memory()
-                    for _ in range(e2e_steps + 1)]
+        ids_host = [torch.from_numpy(rng.integers(0, E, size=(L, routed), dtype=np.int32))
+                    .pin_memory() for _ in range(n_e2e + 1)]
         ids_dev = torch.empty((L, routed), dtype=torch.int32, device=dev)
-        # first D2H into a freshly pinned buffer runs slow (IOMMU/page-table
-        # warm-up): touch every host buffer once before timing
-        for hb in eng.host:
-            if hb is not None:
-                n_ = min(hb.numel(), eng.staging.numel())
-                hb[:n_].copy_(eng.staging[:n_])
-        h2d = d2h = 0
-        base_it = args.warmup + args.steps + 10
+        base_it = 10 ** 6
 
         def e2e_step(k, it):
-            nonlocal h2d, d2h
-            ids_dev.copy_(ids_host[k], non_blocking=True)
-            h2d += ids_host[k].numel() * 4
+            ids_dev.copy_(ids_host[k], non_blocking=True)          # H2D of the step's input
             counters.add_iteration(ids_dev)
-            buf = ck.checkpoint(it)               # select + plan + pack + drain
-            ck.wait_snapshot(buf)                 # wait for SNAPSHOTTED
+            buf = ck.checkpoint(it)                                 # select + plan + pack + drain
+            ck.wait_snapshot(buf)                                   # SNAPSHOTTED: bytes in RAM
             first = eng.snapshot_layout(buf, rank).entries[0]
-            _ = int(eng.entry_view(buf, rank, first.store_key)[0])  # host read
-            d2h += eng.snapshot_nbytes(buf)
+            _ = int(eng.entry_view(buf, rank, first.store_key)[0])  # host read of the result
+            return ids_host[k].numel() * 4, eng.snapshot_nbytes(buf)
 
-        # one untimed step through the same calls (first-call host costs), then
-        # its persist drains before the timed steps
-        if warm_e2e:
-            e2e_step(e2e_steps, base_it - args.i_ckpt)
-            ck.finish()
-        h2d = d2h = 0
-        n_persist0 = len(eng.stats["persist_s"])
+        e2e_step(n_e2e, base_it)                  # untimed: first-call host costs
         barrier(world)
         torch.cuda.synchronize()
-        ck.hold_persist(True)   # measure the snapshot tier alone; persist after
+        h2d = d2h = 0
         tw = time.perf_counter()
-        for k in range(e2e_steps):
-            e2e_step(k, base_it + k)
-        e2e_s = time.perf_counter() - tw
-        e2e_s = max_over_ranks(e2e_s, world, dev)
-        e2e_moved = sum_over_ranks(sum(eng.stats["snap_bytes"][-e2e_steps:]), world, dev)
+        for k in range(n_e2e):
+            hb, db = e2e_step(k, base_it + 1 + k)
+            h2d += hb
+            d2h += db
+        e2e_s = max_over_ranks(time.perf_counter() - tw, world, dev)
+        e2e_moved = sum_over_ranks(sum(eng.stats["snap_bytes"][-n_e2e:]), world, dev)
+        drains = eng.stats["drain_ms"][-n_e2e:]
         e2e = {"value": round(e2e_moved / e2e_s / 1e9, 3), "unit": UNIT,
-               "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
-               "steps": e2e_steps, "ms_per_step": round(e2e_s / e2e_steps * 1e3, 2),
-               "drain_ms": [round(x, 2) for x in eng.stats["drain_ms"][-e2e_steps:]],
-               "what": "router-id H2D + count + select + pack + D2H drain to pinned host",
+               "h2d_bytes_per_step": h2d // n_e2e, "d2h_bytes_per_step": d2h // n_e2e,
+               "steps": n_e2e, "ms_per_step": round(e2e_s / n_e2e * 1e3, 2),
+               "drain_ms": [round(x, 2) for x in drains],
+               "what": "router-id H2D + count + select + pack(+CRC) + D2H drain to pinned host "
+                       "+ host read, through PecCheckpointer (snapshot tier)",
                "host_pin_s": round(pin_s, 1)}
-        tp0 = time.perf_counter()
-        ck.finish()
-        timed_persist = eng.stats["persist_s"][n_persist0:]
-        if store is not None and timed_persist:
-            persisted = sum(eng.stats["snap_bytes"][-e2e_steps:])
+        drain_gbs = statistics.mean([(d2h // n_e2e) / (m / 1e3) / 1e9 for m in drains])
+        e2e["per_gpu"] = round(e2e["value"] / world, 3)
+        link_ref = link_conc if world > 1 else link_alone
+        e2e["frac_of_host_link"] = round(e2e["per_gpu"] / link_ref, 4)
+        host_link = {"achieved": round(drain_gbs, 2), "peak": round(link_alone, 2),
+                     "unit": "GB/s",
+                     "peak_kind": "measured in this run: 1 GiB pinned D2H in the drain's "
+                                  "256 MiB pieces on its copy stream, best of 5, this GPU alone",
+                     "peak_all_gpus_concurrent": round(link_conc, 2),
+                     "frac": round(drain_gbs / link_alone, 4),
+                     "frac_of_concurrent": round(drain_gbs / link_conc, 4)}
+
+        # ---- persist probe: one version, this run's persist rate --------------
+        if store is not None:
+            ck.set_persist(True)
+            ck.checkpoint(base_it + n_e2e + 1)
+            ck.finish()
+            p_s = eng.stats["persist_s"][-1]
             persist_info = {"target": persist, "direct_io": bool(args.direct_io),
-                            "versions": len(timed_persist),
-                            "seconds": [round(x, 2) for x in timed_persist],
-                            "GBps": round(persisted / max(sum(timed_persist), 1e-9) / 1e9, 2)}
-    stall = None
-    if not args.no_stall:
-        prune_store(store)
-        stall = measure_stall(ck, arena, dev, args.stall_iters, args.i_ckpt, args.fb_ms)
-        stall["exposed_ms_per_iter"] = round(max_over_ranks(stall["exposed_ms_per_iter"],
-                                                            world, dev), 3)
+                            "crc": "device (pack)" if mode == D.MODE_CRC else "host",
+                            "seconds": round(p_s, 3),
+                            "GBps": round(eng.stats["snap_bytes"][-1] / p_s / 1e9, 2)}
+            if rank == 0:
+                prune_store(store)
+
+        # ---- the cadence the policy derives from this run's measurements ------
+        if store is not None and not args.no_stall:
+            cl = replace(layout.cluster,
+                         snapshot_bandwidth=min_over_ranks(pack_bw, world, dev),
+                         persist_bandwidth=min_over_ranks(
+                             eng.stats["snap_bytes"][-1] / eng.stats["persist_s"][-1],
+                             world, dev),
+                         fb_time=args.fb_ms / 1e3, update_time=args.update_ms / 1e3)
+            dbw = min_over_ranks(drain_bandwidth(eng.stats), world, dev)
+            cad = b200_cadence(layout, w.strategy, w.pec, cl, dbw)
+            cadence = {"i_ckpt_requested": args.i_ckpt, "i_ckpt_min": cad.i_ckpt_min,
+                       "feasible": cad.i_ckpt_min <= args.i_ckpt,
+                       "floors": {"persist": cad.persist_floor, "drain": cad.drain_floor,
+                                  "snapshot_overlap": cad.snapshot_floor},
+                       "persist_s": round(cad.persist_s, 3), "drain_s": round(cad.drain_s, 3),
+                       "pack_ms": round(cad.pack_s * 1e3, 3),
+                       "measured_GBps": {"pack": round(cl.snapshot_bandwidth / 1e9, 1),
+                                         "drain": round(dbw / 1e9, 2),
+                                         "persist": round(cl.persist_bandwidth / 1e9, 2)},
+                       "what": "policy.b200_cadence on this run's slowest-rank pack / drain / "
+                               "persist rates, F&B + update proxy times"}
+            try:
+                free = b200_configure(layout, w.strategy, cl, dbw)
+                cadence["policy_free_choice"] = {"k_snapshot": free.pec.k_snapshot,
+                                                 "k_persist": free.pec.k_persist,
+                                                 "i_ckpt": free.i_ckpt}
+            except Exception as exc:  # informational only
+                cadence["policy_free_choice"] = {"error": str(exc)[:120]}
+
+    if not args.no_stall and store is not None:
+        i_ckpt = max(args.i_ckpt, cadence["i_ckpt_min"]) if cadence else args.i_ckpt
+        if cadence and not cadence["feasible"]:
+            print(f"bench: I_ckpt={args.i_ckpt} is infeasible on this box (persist/drain "
+                  f"floor {cadence['i_ckpt_min']}); the stall leg runs at I_ckpt={i_ckpt}",
+                  file=sys.stderr)
+        stall = measure_stall(ck, arena, dev, i_ckpt, args.stall_checkpoints, args.fb_ms,
+                              args.stall_rounds, world, rank)
+        if cadence:
+            stall["cadence"] = cadence
     ck.close()
-    if store_root:
+    barrier(world)
+    if store_root and rank == 0:
         shutil.rmtree(store_root, ignore_errors=True)
 
-    # ---- CPU baseline (rank 0, N == 1 only) ----------------------------------
+    # ---- CPU baseline (rank 0, N == 1 only): the reference arm's pack --------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
-        if plan is not None:
-            first_layout = eng.layouts_for(plan.assignments[0], ("phase", 0))[rank]
-        else:
-            first_layout = StagingLayout.build(pt.select({m: frozenset({m % E})
-                                                          for m in range(L)}), arena, rank)
-        gbs, desc = cpu_pack_sample(first_layout.entries, int(args.cpu_sample_gb * 1e9), threads,
-                                    args.cpu_seconds)
-        cpu = {"value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": desc, "cpu_model": cpu_model()}
         try:
-            cpu["components"] = cpu_components(layout, w.strategy, w.pec.k_pec)
+            times, payload, desc, ref, rlayout = cpu_pack_shards(
+                w, 1, 1, 1, threads, int(args.cpu_sample_gb * 1e9) if args.cpu_sample_gb
+                else 0, min_seconds=args.cpu_seconds)
+            cpu = {"value": round(payload / statistics.mean(times) / 1e9, 3), "unit": UNIT,
+                   "cores": threads, "kind": "port", "sample": desc, "cpu_model": cpu_model()}
+            cpu["components"] = reference_components(ref, rlayout, w) if ref is not None \
+                else {"error": "reference not importable"}
         except Exception as exc:  # reported, never fatal to the bench line
-            cpu["components"] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+            cpu = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
     if rank == 0:
         line = {
@@ -722,6 +869,9 @@ def run_b200(args):
                        "bytes_per_step_rank0": moved // args.steps,
                        "state_resident_gb": round(arena.resident_bytes() / 1e9, 2),
                        "engine": args.engine, "chunk_log2": args.chunk_log2,
+                       "value_is": "HBM-staged snapshot: selection + pack (+ per-entry CRC-32C) "
+                                   "into HBM staging, the training-blocking step; e2e = bytes "
+                                   "in pinned host memory (the reference's SNAPSHOTTED)",
                        "l2": (f"no flush needed: each step reads "
                               f"{(moved // args.steps) / 1e9:.2f} GB (> 126 MB L2)"
                               if flush is None else
@@ -736,16 +886,11 @@ def run_b200(args):
                          # figure (7.7 TB/s, B200_PROFILING.md) bounds both
                          "nominal": HBM_NOMINAL_GBS,
                          "frac_of_nominal": round(achieved / HBM_NOMINAL_GBS, 4),
-                         "kernel": f"pec_pack ({args.engine})",
+                         "kernel": f"pec_pack{'_crc' if args.engine == 'crc' else ''} "
+                                   f"({args.engine})",
                          "avg_launch_ms": round(avg_pack_ms, 4)},
             "e2e": e2e,
-            "host_link": ({"achieved": round(statistics.mean(
-                              [e2e["d2h_bytes_per_step"] / (m / 1e3) / 1e9 for m in e2e["drain_ms"]]), 2),
-                           "peak": round(link_alone, 2), "unit": "GB/s",
-                           "peak_kind": "measured in this run: 1 GiB pinned D2H, this GPU alone, "
-                                        "best of 3",
-                           "peak_all_gpus_concurrent": round(link_conc, 2)}
-                          if e2e else None),
+            "host_link": host_link,
             "persist": persist_info,
             "stall": stall,
             "cpu_baseline": cpu,
@@ -757,13 +902,6 @@ def run_b200(args):
                              (3 if args.engine == "crc" else 1)) * args.steps,
             "fill_s": round(t_fill, 2),
         }
-        if line["host_link"]:
-            hl = line["host_link"]
-            hl["frac"] = round(hl["achieved"] / link_alone, 4)
-            hl["frac_of_concurrent"] = round(hl["achieved"] / link_conc, 4)
-            # e2e is bounded by the host link every GPU drains through at once
-            e2e["per_gpu"] = round(e2e["value"] / world, 3)
-            e2e["frac_of_host_link"] = round(e2e["per_gpu"] / link_conc, 4)
         emit(line)
     if world > 1:
         import torch.distributed as dist
@@ -802,7 +940,7 @@ def main():
                          "the persist tier then never reads payloads for checksums), plain "
                          "TMA bulk, or LDG/STG vector")
     ap.add_argument("--chunk-log2", type=int, default=15)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--persist", default="auto", choices=["auto", "none", "shm", "disk"])
     ap.add_argument("--direct-io", action="store_true",
                     help="persist with O_DIRECT (meaningful with --persist disk)")
@@ -811,10 +949,15 @@ def main():
     ap.add_argument("--no-stall", action="store_true")
     ap.add_argument("--no-pipelined-drain", action="store_true",
                     help="drain each snapshot only after its whole pack (A/B of the default)")
-    ap.add_argument("--stall-iters", type=int, default=40)
     ap.add_argument("--i-ckpt", type=int, default=10)
+    ap.add_argument("--stall-checkpoints", type=int, default=12,
+                    help="checkpoints per checkpointed arm (>= 4 triple-buffer cycles)")
+    ap.add_argument("--stall-rounds", type=int, default=2)
     ap.add_argument("--fb-ms", type=float, default=100.0)
-    ap.add_argument("--cpu-sample-gb", type=float, default=2.0)
+    ap.add_argument("--update-ms", type=float, default=25.0,
+                    help="update time the policy assumes (the proxy's pass over the arena)")
+    ap.add_argument("--cpu-sample-gb", type=float, default=0.0,
+                    help="cap per rank for the CPU pack (0 = the full shard, same config)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":

@@ -167,3 +167,43 @@ def b200_configure(layout: RankLayout, strategy: str, cluster: ClusterSpec,
     iter_us = _us(cluster.fb_time) + _us(cluster.update_time)
     drain_floor = max(1, math.ceil(transfer_us(worst, drain_bw) / iter_us))
     return replace(cfg, i_ckpt=max(cfg.i_ckpt, drain_floor))
+
+
+@dataclass(frozen=True)
+class Cadence:
+    """The checkpoint cadence a fixed PEC configuration can sustain."""
+    i_ckpt_min: int          # smallest interval at which nothing queues up
+    persist_floor: int       # ceil(bottleneck persist time / iteration)
+    drain_floor: int         # ceil(bottleneck drain time / iteration)
+    snapshot_floor: int      # ceil(bottleneck pack time / F&B time) (the reference's overlap rule)
+    persist_s: float
+    drain_s: float
+    pack_s: float
+
+
+def b200_cadence(layout: RankLayout, strategy: str, pec: PecConfig, cluster: ClusterSpec,
+                 drain_bw: float) -> Cadence:
+    """For a FIXED K_snapshot / K_persist (a workload's PEC config), the
+    smallest I_ckpt whose steady state never waits: the reference's persist
+    floor (one persist at a time, oldest first: the persist of a version
+    must end before the next one is due, simulator.py:735, engine.py:122-129),
+    the staging floor (the drain must empty staging before the next pack),
+    and the snapshot-overlap rule (simulator.py:434-438).  Bandwidths are the
+    measured ones of `measured_cluster` / `drain_bandwidth`."""
+    strat = EQUAL_PEC if strategy == EQUAL_PEC else ADAPTIVE_PEC
+    snap = PecConfig(k_pec=pec.k_snapshot, k_snapshot=pec.k_snapshot, k_persist=pec.k_snapshot)
+    pers = PecConfig(k_pec=pec.k_persist, k_snapshot=pec.k_persist, k_persist=pec.k_persist)
+
+    def worst(cfg: PecConfig) -> int:
+        plan = plan_equal(layout, cfg) if strat == EQUAL_PEC else plan_adaptive(layout, cfg)
+        return max(bottleneck_workload(plan, p)[1] for p in range(plan.period))
+
+    w_snap, w_pers = worst(snap), worst(pers)
+    iter_us = _us(cluster.fb_time) + _us(cluster.update_time)
+    persist_us = transfer_us(w_pers, cluster.persist_bandwidth)
+    drain_us = transfer_us(w_snap, drain_bw)
+    pack_us = transfer_us(w_snap, cluster.snapshot_bandwidth)
+    pf = max(1, math.ceil(persist_us / iter_us))
+    df = max(1, math.ceil(drain_us / iter_us))
+    sf = max(1, math.ceil(pack_us / max(1, _us(cluster.fb_time))))
+    return Cadence(max(pf, df, sf), pf, df, sf, persist_us / US, drain_us / US, pack_us / US)

@@ -826,7 +826,12 @@ class PecCheckpointer:
         self.async_persist = async_persist
         self.persist_sel: Dict[int, Dict[int, frozenset]] = _PersistSelections(self)
         self._plan: Optional[ShardPlan] = None
+        # host time spent waiting at checkpoints: for the previous snapshot's
+        # drain ("snap") and for a persist to free a buffer ("buffer": the
+        # reference charges NoFreeBufferError as a stall, simulator.py:413-422)
         self.stall_s = 0.0
+        self.waits = {"snap": [0, 0.0], "buffer": [0, 0.0]}
+        self._persist_off = False
         # cumulative delivered tokens of the current timeline at every
         # checkpoint iteration (for the counter reset after a recovery)
         self._cum_at: Dict[int, object] = {}
@@ -934,14 +939,14 @@ class PecCheckpointer:
                 if snapping is not None:
                     t0 = time.perf_counter()
                     self._complete(snapping)
-                    self.stall_s += time.perf_counter() - t0
+                    self._waited("snap", time.perf_counter() - t0)
                 buf = self.engine.begin_snapshot(iteration, c, assignment, plan_key=key)
                 break
             except NoFreeBufferError:
                 t0 = time.perf_counter()
                 if not self._wait_one_persist():
                     raise
-                self.stall_s += time.perf_counter() - t0
+                self._waited("buffer", time.perf_counter() - t0)
         self.persist_sel[buf.version] = persist_sel
         return buf
 
@@ -952,13 +957,13 @@ class PecCheckpointer:
             if snapping is not None:
                 t0 = time.perf_counter()
                 self._complete(snapping)
-                self.stall_s += time.perf_counter() - t0
+                self._waited("snap", time.perf_counter() - t0)
             if any(b.status == "free" for b in self.engine.buffers.buffers):
                 break
             t0 = time.perf_counter()
             if not self._wait_one_persist():
                 raise NoFreeBufferError("no free buffer and no persist in flight")
-            self.stall_s += time.perf_counter() - t0
+            self._waited("buffer", time.perf_counter() - t0)
         snap_d, pers_d = self.counters.select(self.pec.k_snapshot, self.pec.k_persist,
                                               group=self.group)
         return self.engine.begin_snapshot_device(iteration, c, snap_d, pers_d)
@@ -1086,6 +1091,17 @@ class PecCheckpointer:
         self._replay_offset = self.counters.delivered - base
         self._cum_at = {k: v for k, v in self._cum_at.items() if k <= restart}
 
+    def _waited(self, kind: str, seconds: float) -> None:
+        self.stall_s += seconds
+        self.waits[kind][0] += 1
+        self.waits[kind][1] += seconds
+
+    def set_persist(self, enabled: bool) -> None:
+        """Switch the persist tier off (snapshot tier only: completed
+        snapshots become the in-memory recovery copy and buffers recycle
+        without writes) or back on (later snapshots persist again)."""
+        self._persist_off = not enabled
+
     def wait_pack(self, stream=None) -> None:
         self.engine.wait_pack(stream=stream)
 
@@ -1112,9 +1128,10 @@ class PecCheckpointer:
     def _start_persist(self, buf: Buffer) -> None:
         if getattr(self, "_persist_held", False) and self.engine.store is not None:
             return  # stays PERSISTING (queued) until hold_persist(False)
-        if self.engine.store is None:
-            # snapshot tier only (no persist tier configured): the buffer is
-            # published to the in-memory recovery role without any writes
+        if self.engine.store is None or self._persist_off:
+            # snapshot tier only (no persist tier configured, or switched
+            # off): the buffer is published to the in-memory recovery role
+            # without any writes
             nxt = self.engine.buffers.complete_persist(buf)
             if nxt is not None:
                 self._start_persist(nxt)
