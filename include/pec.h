@@ -185,12 +185,14 @@ int pec_crc32c_many(const void* base, const uint64_t* offs,
 /* ---- native persist writer -------------------- *
  * Replaces: the entry-file loop of DiskStore.write_version (store.py:210-216).
  * Writes file i = lens[i] bytes from host buffer bufs[i] with a pool of up to
- * `threads` threads (whole files per thread, largest first, 4 MiB writes);
- * with crc_out != NULL also returns each file's CRC-32C, computed per piece
- * right after writing it.  flags bit 0: fsync each file; bit 1: O_DIRECT
- * (4 KiB-aligned bounce buffer, last block zero-padded then truncated back;
- * buffered where the filesystem refuses O_DIRECT).  PEC_E_IO on any
- * open/write/fsync/truncate/close failure. */
+ * `threads` threads (whole files per thread, largest first, 4 MiB pwrites;
+ * with O_DIRECT, files above 64 MiB are split into 64 MiB ranges written by
+ * different threads at their offsets); with crc_out != NULL also returns
+ * each file's CRC-32C, computed per piece right after writing it.  flags
+ * bit 0: fsync each file; bit 1: O_DIRECT (4 KiB-aligned bounce buffer, last
+ * block zero-padded then truncated back; buffered where the filesystem
+ * refuses O_DIRECT); bit 2: writer threads at background priority (nice
+ * +10).  PEC_E_IO on any open/write/fsync/truncate/close failure. */
 int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
                     int n, uint32_t* crc_out, int threads, int flags);
 

@@ -14,6 +14,8 @@
 
 #include <errno.h>
 #include <fcntl.h>
+#include <sys/resource.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -237,18 +239,25 @@ int pec_crc32c_many(const void* base, const uint64_t* offs, const uint64_t* lens
   return PEC_OK;
 }
 
-// Native persist writer: file i receives lens[i] bytes from bufs[i].  A pool
-// of threads takes whole files, largest first (tmpfs/ext4 serialise writers
-// of one inode, so files, not byte ranges, are the unit of parallelism), and
-// writes each sequentially in 4 MiB pieces; unless crc_out is NULL each piece
-// is checksummed right after it is written, while it is still cache-hot, so
-// the payload is read once for both.
+// Native persist writer: file i receives lens[i] bytes from bufs[i].
+// Work items are whole files, largest first (tmpfs and buffered ext4
+// serialise writers of one inode, so files are the unit of parallelism
+// there), except that with O_DIRECT a file above kRange is cut into kRange
+// byte ranges written by different threads with pwrite at their offsets
+// (real storage takes parallel direct writes to one file: NVMe queue depth).
+// Files are created/truncated once, before any item runs.  Unless crc_out is
+// NULL every 4 MiB piece is checksummed right after it is written, while it
+// is still cache-hot (ranges' CRCs are combined in order), so the payload is
+// read once for both.
 // flags bit 0: fsync every file before returning.
 // flags bit 1: O_DIRECT (page-cache bypass for real storage): each piece is
 //   copied into a 4 KiB-aligned per-thread bounce buffer (checksummed there,
 //   cache-hot), the last piece is zero-padded to the 4 KiB block and the file
 //   is truncated back to its exact length.  Filesystems that refuse O_DIRECT
 //   (EINVAL, e.g. tmpfs) get the buffered path for that file.
+// flags bit 2: background priority: the writer threads run at nice +10, so
+//   a persist never competes on equal terms with the training loop's
+//   launch thread for host cores (the caller's own thread is not touched).
 int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
                     int n, uint32_t* crc_out, int threads, int flags) {
   if (n < 0 || (n > 0 && (paths == nullptr || bufs == nullptr || lens == nullptr)))
@@ -257,15 +266,44 @@ int pec_write_files(const char* const* paths, const void* const* bufs, const uin
   if (threads < 1) threads = 1;
   constexpr uint64_t kPiece = 4ull << 20;
   constexpr uint64_t kBlock = 4096;
+  constexpr uint64_t kRange = 64ull << 20;
+  const bool want_direct = (flags & 2) != 0;
+
+  // create / truncate every file once; note which accept O_DIRECT
+  std::vector<char> direct_ok(n, 0);
+  for (int i = 0; i < n; ++i) {
+    const int fd = open(paths[i], O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
+    if (fd < 0 || close(fd) != 0) return PEC_E_IO;
+    if (want_direct) {
+      const int dfd = open(paths[i], O_WRONLY | O_CLOEXEC | O_DIRECT);
+      if (dfd >= 0) {
+        direct_ok[i] = 1;
+        close(dfd);
+      } else if (errno != EINVAL) {
+        return PEC_E_IO;
+      }
+    }
+  }
+  struct Item { int file; uint64_t off, len; uint32_t crc; };
   std::vector<int> order(n);
   for (int i = 0; i < n; ++i) order[i] = i;
   std::sort(order.begin(), order.end(), [&](int a, int b) { return lens[a] > lens[b]; });
-  std::atomic<int> next{0};
+  std::vector<Item> items;
+  for (int i : order) {
+    const uint64_t step = (direct_ok[i] && lens[i] > kRange) ? kRange : lens[i];
+    uint64_t o = 0;
+    do {
+      const uint64_t l = std::min<uint64_t>(step ? step : 0, lens[i] - o);
+      items.push_back(Item{i, o, l, 0});
+      o += l;
+    } while (o < lens[i]);
+  }
+  std::atomic<size_t> next{0};
   std::atomic<int> failed{0};
-  auto write_all = [](int fd, const uint8_t* p, uint64_t len) {
+  auto pwrite_all = [](int fd, const uint8_t* p, uint64_t len, uint64_t at) {
     uint64_t done = 0;
     while (done < len) {
-      const ssize_t w = write(fd, p + done, len - done);
+      const ssize_t w = pwrite(fd, p + done, len - done, (off_t)(at + done));
       if (w < 0) {
         if (errno == EINTR) continue;
         return false;
@@ -275,23 +313,14 @@ int pec_write_files(const char* const* paths, const void* const* bufs, const uin
     return true;
   };
   auto work = [&]() {
-    uint8_t* bounce = nullptr;  // per-thread, allocated on first O_DIRECT file
-    for (int k = next.fetch_add(1); k < n; k = next.fetch_add(1)) {
+    if (flags & 4) setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), 10);
+    uint8_t* bounce = nullptr;  // per-thread, allocated on first O_DIRECT item
+    for (size_t k = next.fetch_add(1); k < items.size(); k = next.fetch_add(1)) {
       if (failed.load()) break;
-      const int i = order[k];
-      const int base = O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC;
-      int fd = -1;
-      bool direct = false;
-      if (flags & 2) {
-        fd = open(paths[i], base | O_DIRECT, 0644);
-        if (fd >= 0) {
-          direct = true;
-        } else if (errno != EINVAL) {
-          failed.store(1);
-          break;
-        }
-      }
-      if (fd < 0) fd = open(paths[i], base, 0644);
+      Item& it = items[k];
+      const int i = it.file;
+      const bool direct = direct_ok[i] != 0;
+      const int fd = open(paths[i], O_WRONLY | O_CLOEXEC | (direct ? O_DIRECT : 0));
       if (fd < 0) {
         failed.store(1);
         break;
@@ -306,36 +335,52 @@ int pec_write_files(const char* const* paths, const void* const* bufs, const uin
       const uint8_t* src = static_cast<const uint8_t*>(bufs[i]);
       uint32_t crc = 0;
       bool ok = true;
-      for (uint64_t off = 0; off < lens[i] && ok; off += kPiece) {
-        const uint64_t len = std::min<uint64_t>(kPiece, lens[i] - off);
+      const uint64_t end = it.off + it.len;
+      for (uint64_t off = it.off; off < end && ok; off += kPiece) {
+        const uint64_t len = std::min<uint64_t>(kPiece, end - off);
         if (direct) {
           std::memcpy(bounce, src + off, len);
           if (crc_out != nullptr) crc = crc_impl(bounce, len, crc);
           const uint64_t padded = (len + kBlock - 1) / kBlock * kBlock;
           if (padded > len) std::memset(bounce + len, 0, padded - len);
-          ok = write_all(fd, bounce, padded);
+          ok = pwrite_all(fd, bounce, padded, off);
         } else {
-          ok = write_all(fd, src + off, len);
+          ok = pwrite_all(fd, src + off, len, off);
           if (ok && crc_out != nullptr) crc = crc_impl(src + off, len, crc);
         }
       }
-      if (ok && direct && lens[i] % kBlock != 0 && ftruncate(fd, (off_t)lens[i]) != 0) ok = false;
+      // the range holding the file's end trims the padded last block
+      if (ok && direct && end == lens[i] && lens[i] % kBlock != 0 &&
+          ftruncate(fd, (off_t)lens[i]) != 0)
+        ok = false;
       if (ok && (flags & 1) && fsync(fd) != 0) ok = false;
       if (close(fd) != 0) ok = false;
       if (!ok) {
         failed.store(1);
         break;
       }
-      if (crc_out != nullptr) crc_out[i] = crc;
+      it.crc = crc;
     }
     free(bounce);
   };
-  const int nt = std::min(threads, n);
+  const int nt = (int)std::min<size_t>((size_t)threads, items.size());
   std::vector<std::thread> pool;
-  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
-  work();
+  pool.reserve(nt);
+  for (int t = 0; t < nt; ++t) pool.emplace_back(work);
   for (auto& th : pool) th.join();
-  return failed.load() ? PEC_E_IO : PEC_OK;
+  if (failed.load()) return PEC_E_IO;
+  if (crc_out != nullptr) {
+    // ranges of a file are consecutive items (planned in file order)
+    size_t k = 0;
+    while (k < items.size()) {
+      const int i = items[k].file;
+      uint32_t c = 0;
+      for (; k < items.size() && items[k].file == i; ++k)
+        c = combine_impl(c, items[k].crc, items[k].len);
+      crc_out[i] = c;
+    }
+  }
+  return PEC_OK;
 }
 
 }  // extern "C"

@@ -352,11 +352,12 @@ def crc32c_many(base, offsets, lengths, threads: Optional[int] = None) -> np.nda
 
 
 def write_files(paths, buffers, threads: Optional[int] = None, want_crc: bool = True,
-                fsync: bool = False, direct: bool = False):
+                fsync: bool = False, direct: bool = False, background: bool = False):
     """Native multi-threaded writer (pec_write_files): file i <- buffers[i]
     (bytes-like / ndarray / CPU tensor).  Returns the CRC-32C of each file
     (uint32 ndarray) when ``want_crc``.  ``direct`` opens files O_DIRECT
-    (page-cache bypass; buffered where the filesystem refuses it)."""
+    (page-cache bypass; buffered where the filesystem refuses it; large files
+    range-parallel); ``background`` runs the writer threads at nice +10."""
     n = len(paths)
     keep = [_host_buffer(b) for b in buffers]
     c_paths = (ctypes.c_char_p * n)(*[os.fsencode(str(p)) for p in paths])
@@ -369,7 +370,8 @@ def write_files(paths, buffers, threads: Optional[int] = None, want_crc: bool = 
                                ctypes.cast(c_bufs, ctypes.c_void_p),
                                lens.ctypes.data if n else None, n,
                                out.ctypes.data if want_crc and n else None, int(threads),
-                               (1 if fsync else 0) | (2 if direct else 0))
+                               (1 if fsync else 0) | (2 if direct else 0) |
+                               (4 if background else 0))
     _check(rc, "pec_write_files")
     del keep
     return out

@@ -191,16 +191,21 @@ def _fsync_path(path) -> None:
 class DiskStore:
     """One directory per version under ``root`` (store.py:171-282)."""
 
-    def __init__(self, root, io_threads: int = 8, direct_io: bool = False, fsync: bool = False):
+    def __init__(self, root, io_threads: int = 8, direct_io: bool = False, fsync: bool = False,
+                 background: bool = True):
         """B200 additions: ``io_threads`` for the native writer/reader,
         ``direct_io`` writes real payloads with O_DIRECT (page-cache bypass
-        on real storage; buffered where the filesystem refuses it), ``fsync``
-        makes every entry file durable before the version is published."""
+        on real storage, large files range-parallel; buffered where the
+        filesystem refuses it), ``fsync`` makes every entry file durable
+        before the version is published, ``background`` runs the writer
+        threads at nice +10 (a persist yields host cores to the training
+        loop's launch thread)."""
         self.root = Path(root)
         self.root.mkdir(parents=True, exist_ok=True)
         self.io_threads = max(1, io_threads)
         self.direct_io = direct_io
         self.fsync = fsync
+        self.background = background
 
     def version_dir(self, version: int) -> Path:
         return self.root / f"v{version:06d}"
@@ -250,7 +255,8 @@ class DiskStore:
             # each 4 MiB piece right after writing it
             paths = [vdir / _entry_path(e.rank, e.store_key) for e in entries]
             got = _dev.write_files(paths, data, threads=self.io_threads, want_crc=not given,
-                                   fsync=self.fsync, direct=self.direct_io)
+                                   fsync=self.fsync, direct=self.direct_io,
+                                   background=self.background)
             crc_list = [crcs[e.store_key] for e in entries] if given else [int(c) for c in got]
             return [(e.store_key, _entry_path(e.rank, e.store_key), _nbytes(p), c)
                     for e, p, c in zip(entries, data, crc_list)]

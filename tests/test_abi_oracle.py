@@ -114,8 +114,13 @@ def test_native_writer_writes_exact_bytes_and_crcs(tmp_path, direct, fsync):
     bufs = [rng.integers(0, 256, size=n, dtype=np.uint8)
             for n in (0, 1, 4096, 4097, (4 << 20) + 5, (8 << 20))]
     bufs.append(bufs[3][3:])  # unaligned source address
+    # O_DIRECT splits files above 64 MiB into ranges written by different
+    # threads at their offsets (CRCs of the ranges combined in order)
+    bufs.append(rng.integers(0, 256, size=(150 << 20) + 12_345, dtype=np.uint8))
+    bufs.append(bufs[-1][1:(128 << 20) + 1])   # exactly two ranges, unaligned source
     paths = [tmp_path / f"e{i}.bin" for i in range(len(bufs))]
-    crcs = D.write_files(paths, bufs, threads=3, direct=direct, fsync=fsync)
+    crcs = D.write_files(paths, bufs, threads=3, direct=direct, fsync=fsync,
+                         background=direct)
     for p, b, c in zip(paths, bufs, crcs):
         assert p.read_bytes() == b.tobytes()
         assert int(c) == crc32c(b)
