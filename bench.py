@@ -613,8 +613,8 @@ def run_b200(args):
             import torch.distributed as dist
             dist.broadcast_object_list(root, src=0)
         store_root = root[0]
-        store = DiskStore(store_root, io_threads=len(os.sched_getaffinity(0)),
-                          direct_io=args.direct_io)
+        store = DiskStore(store_root, io_threads=args.persist_threads or
+                          len(os.sched_getaffinity(0)), direct_io=args.direct_io)
     mode = {"vec": D.MODE_VEC, "bulk": D.MODE_BULK, "crc": D.MODE_CRC}[args.engine]
     # the persist protocol gets its own gloo group (created collectively inside)
     ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=1, ranks=[rank],
@@ -833,8 +833,11 @@ def run_b200(args):
             print(f"bench: I_ckpt={args.i_ckpt} is infeasible on this box (persist/drain "
                   f"floor {cadence['i_ckpt_min']}); the stall leg runs at I_ckpt={i_ckpt}",
                   file=sys.stderr)
+        if args.stall_no_persist:
+            ck.set_persist(False)
         stall = measure_stall(ck, arena, dev, i_ckpt, args.stall_checkpoints, args.fb_ms,
                               args.stall_rounds, world, rank)
+        stall["persist_tier"] = "off (diagnostic)" if args.stall_no_persist else "on"
         if cadence:
             stall["cadence"] = cadence
     ck.close()
@@ -944,6 +947,10 @@ def main():
     ap.add_argument("--persist", default="auto", choices=["auto", "none", "shm", "disk"])
     ap.add_argument("--direct-io", action="store_true",
                     help="persist with O_DIRECT (meaningful with --persist disk)")
+    ap.add_argument("--persist-threads", type=int, default=0,
+                    help="writer threads per rank (0 = all host cores; background priority)")
+    ap.add_argument("--stall-no-persist", action="store_true",
+                    help="diagnostic: run the stall leg with the persist tier off")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stall", action="store_true")
