@@ -439,6 +439,35 @@ def prune_store(store, keep: int = 2) -> None:
         shutil.rmtree(store.version_dir(v), ignore_errors=True)
 
 
+class Retention:
+    """`prune_store` on a background thread: freeing a 12.6 GB version's
+    tmpfs pages takes ~0.5 s, which must not block the training thread (a
+    blocked launch thread starves the GPU)."""
+
+    def __init__(self, store, keep: int = 2):
+        import queue
+        self.store, self.keep = store, keep
+        self.q = queue.Queue()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        while True:
+            item = self.q.get()
+            if item is None:
+                return
+            prune_store(self.store, self.keep)
+            self.q.task_done()
+
+    def submit(self):
+        if self.q.empty():
+            self.q.put(1)
+
+    def close(self):
+        self.q.put(None)
+        self.t.join()
+
+
 def measure_host_link(eng, world, dev):
     """Host-link roofline measured in this run, on the drain's own path (the
     copy stream, 256 MiB pieces): 1 GiB pinned D2H, best of 5, each rank
@@ -510,6 +539,7 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
     iters = (n_ckpt + 1) * i_ckpt
     store = ck.engine.store
     stats = ck.engine.stats
+    retention = Retention(store) if (rank == 0 and store is not None) else None
 
     def run(with_ckpt: bool, base_it: int):
         barrier(world)
@@ -517,7 +547,10 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
         w0 = {k: list(v) for k, v in ck.waits.items()}
         p0 = len(stats["persist_s"])
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+        host = {"checkpoint_s": 0.0, "finish_s": 0.0}
         t0.record(compute)
+        marks[0].record(compute)
         for k in range(1, iters + 1):
             it = base_it + k
             for _ in range(n_gemm):                 # forward + backward
@@ -527,26 +560,39 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
                 ck.wait_pack(stream=compute)        # the update may not race the pack
             words.add_(1)                           # optimizer step
             if with_ckpt and k % i_ckpt == 0 and k <= n_ckpt * i_ckpt:
+                h0 = time.perf_counter()
                 ck.checkpoint(it)                   # select + plan + pack + drain
-                if rank == 0:
-                    prune_store(store)
+                host["checkpoint_s"] += time.perf_counter() - h0
+                if retention is not None:
+                    retention.submit()              # bench-only: old versions off /dev/shm
+            marks[k].record(compute)
         if with_ckpt:
+            h0 = time.perf_counter()
             ck.finish()                             # every drain and persist, in the window
+            host["finish_s"] = time.perf_counter() - h0
         t1.record(compute)
         t1.synchronize()
         waits = {k: [ck.waits[k][0] - w0[k][0], ck.waits[k][1] - w0[k][1]] for k in w0}
-        return t0.elapsed_time(t1) / iters, waits, stats["persist_s"][p0:]
+        per_it = [marks[k - 1].elapsed_time(marks[k]) for k in range(1, iters + 1)]
+        top = sorted(range(iters), key=lambda j: -per_it[j])[:6]
+        host["slowest_iters"] = [(j + 1, round(per_it[j], 2)) for j in top]
+        host["median_iter_ms"] = round(statistics.median(per_it), 3)
+        host["tail_ms"] = round(marks[iters].elapsed_time(t1), 2)
+        return t0.elapsed_time(t1) / iters, waits, stats["persist_s"][p0:], host
 
     # checkpoint c = iteration // i_ckpt - 1 walks the plan's phases in order
     ck.i_ckpt = i_ckpt
     run(False, 0)  # warm
-    runs_without, runs_with, waits_all, persists = [], [], [], []
+    runs_without, runs_with, waits_all, persists, hosts = [], [], [], [], []
     for r in range(rounds):
         runs_without.append(run(False, 0)[0])
-        ms, waits, pers = run(True, i_ckpt * 10 ** 6 * (r + 1))
+        ms, waits, pers, host = run(True, i_ckpt * 10 ** 6 * (r + 1))
         runs_with.append(ms)
         waits_all.append(waits)
         persists += pers
+        hosts.append({k: (round(v, 3) if isinstance(v, float) else v) for k, v in host.items()})
+    if retention is not None:
+        retention.close()
     without = max_over_ranks(statistics.mean(runs_without), world, dev)
     with_ = max_over_ranks(statistics.mean(runs_with), world, dev)
     packs = stats["pack_ms"][-rounds * n_ckpt:]
@@ -575,7 +621,8 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
                                   else None,
                                   "GBps": round(shard / statistics.mean(persists) / 1e9, 2)
                                   if persists else None},
-            "window": "every drain and persist of the arm completes inside the timed window"}
+            "window": "every drain and persist of the arm completes inside the timed window",
+            "diag_with_arms": hosts}
 
 
 def run_b200(args):

@@ -1054,7 +1054,10 @@ class PecCheckpointer:
                 if not want:
                     break
                 if v not in metas:
-                    meta = store.meta(v)
+                    try:
+                        meta = store.meta(v)
+                    except (OSError, ValueError, KeyError):
+                        continue        # removed by an external retention policy meanwhile
                     metas[v] = (meta.iteration, {e.unit_key for e in meta.entries.values()})
                 it, units = metas[v]
                 hit = want & units

@@ -62,6 +62,16 @@ case "$recipe" in
       -k regex:"pack_crc|crc_fold|crc_final" -s 3 -c 3 -o $O/prof_crc $CMD > $O/ncu_crc.log 2>&1
     echo ncu=$?
     ;;
+  sanitize)   # compute-sanitizer over every libpec kernel (tools/sanitize_kernels.py)
+    K="--kernel-name kns=pack_crc_kernel --kernel-name kns=crc_fold --kernel-name kns=crc_final"
+    K="$K --kernel-name kns=copy_bulk --kernel-name kns=copy_vec --kernel-name kns=token_hist"
+    K="$K --kernel-name kns=select_ --kernel-name kns=expand_plan"
+    for t in memcheck racecheck synccheck initcheck; do
+      timeout 1500 compute-sanitizer --tool $t $K --print-limit 50 \
+        python tools/sanitize_kernels.py > $O/sanitize_$t.txt 2>&1; echo $t=$?
+      tail -3 $O/sanitize_$t.txt
+    done
+    ;;
   host_link)   # pinned D2H / push probes
     timeout 300 python tools/d2h_probe.py > $O/d2h_probe.json 2>&1; cat $O/d2h_probe.json
     timeout 300 python tools/d2h_push_probe.py > $O/d2h_push_probe.json 2>&1
