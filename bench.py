@@ -120,12 +120,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def dist_backend() -> str:
+    """NCCL (the contract).  PEC_DIST_BACKEND=gloo exists only to exercise
+    the N-rank code path with more ranks than GPUs (ranks then share devices
+    round-robin, which NCCL refuses); it is reported in the line."""
+    return os.environ.get("PEC_DIST_BACKEND", "nccl")
+
+
 def dist_init(n_gpus):
+    import torch
     rank, local, world = env_rank()
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
-        import torch
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dist_backend() == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, local, world
 
 
@@ -140,7 +151,8 @@ def _reduce(x, world, device, op):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64,
+                     device="cpu" if dist_backend() == "gloo" else device)
     dist.all_reduce(t, op=op)
     return float(t.item())
 
@@ -927,7 +939,8 @@ def run_b200(args):
                               if flush is None else
                               "512 MiB L2 flush written between steps, inside the timed "
                               "region (steps move less than 4x the 126 MB L2)"),
-                       "parallelism": f"dp{layout.n_ranks}-ep{layout.parallel.ep_degree}"},
+                       "parallelism": f"dp{layout.n_ranks}-ep{layout.parallel.ep_degree}",
+                       "dist_backend": dist_backend() if world > 1 else None},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                          "traffic": traffic, "peak_kind": peak_kind,
