@@ -171,18 +171,32 @@ def sum_over_ranks(x, world, device):
     return _reduce(x, world, device, dist.ReduceOp.SUM if world > 1 else None)
 
 
-def host_buffers_that_fit(nbytes: int, want: int, frac: float = 0.7) -> int:
-    """How many pinned host snapshot buffers of ``nbytes`` each local rank
-    can take (LOCAL_WORLD_SIZE ranks pin at once) within ``frac`` of the
-    node's MemAvailable."""
+def mem_available() -> int:
     try:
         with open("/proc/meminfo") as f:
             info = {ln.split(":")[0]: int(ln.split()[1]) * 1024 for ln in f if ":" in ln}
-        avail = info.get("MemAvailable", info.get("MemFree", 0))
+        return info.get("MemAvailable", info.get("MemFree", 0))
     except OSError:
+        return 0
+
+
+def host_buffers_that_fit(nbytes: int, want: int, frac: float = 0.7, reserve: int = 0) -> int:
+    """How many pinned host snapshot buffers of ``nbytes`` each local rank
+    can take (LOCAL_WORLD_SIZE ranks pin at once) within ``frac`` of the
+    node's MemAvailable, after ``reserve`` bytes per rank for other uses
+    (the persist tier's /dev/shm versions)."""
+    avail = mem_available()
+    if not avail:
         return want
     local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
-    return max(0, min(want, int(frac * avail // (local * max(1, nbytes)))))
+    per_rank = frac * avail / local - reserve
+    return max(0, min(want, int(per_rank // max(1, nbytes))))
+
+
+# versions of every rank's shard the /dev/shm persist tier holds at once in
+# steady state: the newest complete one (retention keeps 1), one being written,
+# one complete but not yet pruned (retention runs on a background thread)
+SHM_VERSIONS_IN_FLIGHT = 3
 
 
 def cpu_model() -> str:
@@ -441,7 +455,7 @@ def build_workload(args, rank):
     return w, layout, plan
 
 
-def prune_store(store, keep: int = 2) -> None:
+def prune_store(store, keep: int = 1) -> None:
     """Bench-only retention: drop all but the newest ``keep`` complete
     versions (each is a full rank shard; /dev/shm is host RAM)."""
     if store is None or not hasattr(store, "version_dir"):
@@ -456,7 +470,7 @@ class Retention:
     tmpfs pages takes ~0.5 s, which must not block the training thread (a
     blocked launch thread starves the GPU)."""
 
-    def __init__(self, store, keep: int = 2):
+    def __init__(self, store, keep: int = 1):
         import queue
         self.store, self.keep = store, keep
         self.q = queue.Queue()
@@ -522,7 +536,7 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
     pass over the whole state arena: HBM-bound like a fused Adam step over the
     rank's ~85 GB shard).  The checkpointed arm takes ``n_ckpt`` checkpoints,
     one every ``i_ckpt`` iterations after the update, with the persist tier
-    ON (retention keeps the newest 2 versions), then runs one more interval
+    ON (retention keeps the newest complete version), then runs one more interval
     without a checkpoint, then waits for every drain and persist — all inside
     the timed window, so a persist tier that cannot keep up shows as stall.
     The next update always waits for the pending pack.  Arms alternate
@@ -662,6 +676,7 @@ def run_b200(args):
     counters = DeviceTokenCounters(L, E, dev, DeviceTokenCounters.capacity_for(
         w.capacity_factor, [routed] * L, E))
     persist = args.persist if args.persist != "auto" else "shm"
+    persist_dropped = None
     store = None
     store_root = None
     if persist != "none":
@@ -768,7 +783,25 @@ def run_b200(args):
 
     # ---- host buffers: pinned once, before any host-side timing -------------
     tpin = time.perf_counter()
-    fit = host_buffers_that_fit(eng.staging.numel(), 3)
+    # a /dev/shm persist tier holds SHM_VERSIONS_IN_FLIGHT shards per rank in
+    # host RAM next to the pinned buffers; when both do not fit, the persist
+    # tier is dropped (the line says so) rather than the node running out
+    shard = step_bytes
+    shm_reserve = SHM_VERSIONS_IN_FLIGHT * shard if (store is not None and persist == "shm") \
+        else 0
+    fit = host_buffers_that_fit(eng.staging.numel(), 3, reserve=shm_reserve)
+    if store is not None and persist == "shm" and \
+            min_over_ranks(float(fit), world, dev) < 3:
+        fit_np = host_buffers_that_fit(eng.staging.numel(), 3)
+        if min_over_ranks(float(fit_np), world, dev) >= 2:
+            print(f"bench: host RAM ({mem_available() / 1e9:.0f} GB available) cannot hold 3 "
+                  f"pinned buffers + {SHM_VERSIONS_IN_FLIGHT} /dev/shm versions per rank; "
+                  "persist tier off", file=sys.stderr)
+            persist_dropped = f"host RAM: {mem_available() / 1e9:.0f} GB available for " \
+                              f"{os.environ.get('LOCAL_WORLD_SIZE', '1')} ranks"
+            store = None
+            ck.engine.store = None
+            fit = fit_np
     n_host = int(min_over_ranks(float(fit), world, dev))    # node-wide minimum
     pin_error = None
     if n_host < 2:
@@ -787,8 +820,9 @@ def run_b200(args):
         print(f"bench: pinned host buffers unavailable ({pin_error}); skipping the host legs",
               file=sys.stderr)
         args.no_e2e = args.no_stall = True
-    if n_host < 3:
-        args.no_stall = True      # the steady state needs RECOVERY + PERSISTING + SNAPSHOTTING
+    if n_host < (3 if store is not None else 2):
+        # the steady state needs RECOVERY + PERSISTING + SNAPSHOTTING (2 without a persist tier)
+        args.no_stall = True
 
     link_alone = link_conc = None
     e2e = host_link = persist_info = cadence = stall = None
@@ -886,7 +920,7 @@ def run_b200(args):
             except Exception as exc:  # informational only
                 cadence["policy_free_choice"] = {"error": str(exc)[:120]}
 
-    if not args.no_stall and store is not None:
+    if not args.no_stall:
         i_ckpt = max(args.i_ckpt, cadence["i_ckpt_min"]) if cadence else args.i_ckpt
         if cadence and not cadence["feasible"]:
             print(f"bench: I_ckpt={args.i_ckpt} is infeasible on this box (persist/drain "
@@ -896,7 +930,9 @@ def run_b200(args):
             ck.set_persist(False)
         stall = measure_stall(ck, arena, dev, i_ckpt, args.stall_checkpoints, args.fb_ms,
                               args.stall_rounds, world, rank)
-        stall["persist_tier"] = "off (diagnostic)" if args.stall_no_persist else "on"
+        stall["persist_tier"] = "off (diagnostic)" if args.stall_no_persist else \
+            (f"off ({persist_dropped})" if persist_dropped else
+             ("on" if store is not None else "none configured"))
         if cadence:
             stall["cadence"] = cadence
     ck.close()
@@ -954,7 +990,8 @@ def run_b200(args):
                          "avg_launch_ms": round(avg_pack_ms, 4)},
             "e2e": e2e,
             "host_link": host_link,
-            "persist": persist_info,
+            "persist": persist_info if persist_info else
+            ({"off": persist_dropped} if persist_dropped else None),
             "stall": stall,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),

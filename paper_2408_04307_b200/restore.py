@@ -124,7 +124,7 @@ def _pieces(engine, plan: RecoveryPlan, wanted, slot_bytes: int):
                     if peer is None:
                         continue
                     src, st = peer[0].array, peer[1]
-                    base0, kind = 0, "bytes"
+                    base0, kind = peer[2], "bytes"
                 for e in st.entries:
                     if e.unit_key != key:
                         continue

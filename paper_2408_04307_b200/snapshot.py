@@ -178,8 +178,9 @@ class DeviceCheckpointEngine(CheckpointEngine):
                                                    pin_memory=True)
             else:
                 from .hostmem import SharedHostBuffer, buffer_name
-                if len(self.ranks) != 1:
-                    raise ValueError("shared host buffers need one local rank per engine")
+                # one node-shared file per buffer, named by the engine's first
+                # rank; every hosted rank's region is published with its
+                # offset (_publish_meta), so peers map the right bytes
                 old = self._shared.pop(buffer_id, None)
                 self.host[buffer_id] = None
                 if old is not None:
@@ -201,12 +202,15 @@ class DeviceCheckpointEngine(CheckpointEngine):
         import os
         if self.shared_prefix is None:
             return
+        from .hostmem import buffer_name
         for r in rec.layouts:
             path = self._meta_path(r, buf.buffer_id)
             tmp = path + ".tmp"
             with open(tmp, "w") as f:
                 json.dump({"version": buf.version, "iteration": buf.iteration,
-                           "nbytes": rec.nbytes}, f)
+                           "nbytes": rec.layouts[r].nbytes,
+                           "file": buffer_name(self.shared_prefix, self.ranks[0], buf.buffer_id),
+                           "offset": rec.region[r]}, f)
             os.replace(tmp, path)
 
     def _retract_meta(self, buffer_id: int) -> None:
@@ -220,11 +224,11 @@ class DeviceCheckpointEngine(CheckpointEngine):
                 pass
 
     def peer_buffer(self, rank: int, version: int):
-        """(host array, StagingLayout) of peer ``rank``'s in-memory copy of
-        ``version`` on this node, or None."""
+        """(mapped SharedHostBuffer, StagingLayout, region offset) of peer
+        ``rank``'s in-memory copy of ``version`` on this node, or None."""
         import json
         from .arena import PeerSlots
-        from .hostmem import SharedHostBuffer, buffer_name
+        from .hostmem import SharedHostBuffer
         if self.shared_prefix is None:
             return None
         buf = next((b for b in self.buffers.buffers if b.version == version), None)
@@ -238,14 +242,12 @@ class DeviceCheckpointEngine(CheckpointEngine):
                 continue
             if meta.get("version") != version:
                 continue
-            shb = SharedHostBuffer(buffer_name(self.shared_prefix, rank, bid), create=False,
-                                   register=False)
             st = StagingLayout.build(buf.content.get(rank, ()), PeerSlots(self.layout, rank), rank)
-            # the owner publishes its region size (host plans round it up to 256 B)
-            if meta["nbytes"] not in (st.nbytes, (st.nbytes + 255) // 256 * 256):
+            if meta["nbytes"] != st.nbytes:
                 raise RuntimeError(f"peer rank {rank} v{version}: layout size mismatch "
                                    f"({st.nbytes} B vs {meta['nbytes']} B published)")
-            return shb, st
+            shb = SharedHostBuffer(meta["file"], create=False, register=False)
+            return shb, st, int(meta["offset"])
         return None
 
     def reserve(self, nbytes: int, host_buffers: Optional[int] = None) -> None:

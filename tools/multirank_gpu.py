@@ -103,7 +103,7 @@ def main():
     ck = PecCheckpointer(layout, arena, store, pec, "equal_pec", i_ckpt=3, ranks=my_ranks,
                          counters=counters, group=None, control_group=control,
                          async_persist=False,
-                         shared_host_prefix="pec_mr" if R == 1 else None)
+                         shared_host_prefix="pec_mr")
     ck.group = dist.group.WORLD  # the counter all-reduce (NCCL, or gloo when GPUs are shared)
     failed_node = layout.cluster.num_nodes - 1
 
