@@ -195,6 +195,8 @@ __device__ __forceinline__ ChunkRef chunk_ref(const pec_copy_desc* __restrict__ 
   const uint64_t off = (ch - __ldg(&d[i].first_chunk)) << kCrcLg;
   const uint64_t nb = __ldg(&d[i].nbytes);
   r.len = off >= nb ? 0u : (uint32_t)(nb - off < (uint64_t)kChunk ? nb - off : kChunk);
+  // a chunk index past its descriptor's bytes only exists for empty rows
+  PEC_DCHECK(off < nb || nb == 0 || i + 1 == n);
   r.src = reinterpret_cast<const uint8_t*>(__ldg(&d[i].src) + off);
   r.dst = reinterpret_cast<uint8_t*>(__ldg(&d[i].dst) + off);
   r.fast = r.len == (uint32_t)kChunk &&
@@ -301,6 +303,7 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
       if (p_u == kStagesPerChunk) {
         if (q_tail - q_head == (uint32_t)kQueue) return;
         const uint64_t ch = __shfl_sync(0xffffffffu, res, 0);
+        PEC_DCHECK(q_tail - q_head < (uint32_t)kQueue);
         if (ch >= total) {
           exhausted = true;
           return;
@@ -320,6 +323,7 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
         p_u = 0;
       }
       const int s = (int)(issued % kRing);
+      PEC_DCHECK(issued + 2 <= consumed + kRing && p_u < kStagesPerChunk && p_ref.fast);
       if (lane == 0) {
         if (kStore) bulk_wait_read1();   // the store that last read this stage
         mbar_expect_tx(&my_bars[s], kStage);
@@ -399,8 +403,10 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
       }
       x = c;
     }
+    PEC_DCHECK(ch < total_cap);
     if (lane == 0) chunk_raw[ch] = x;
   }
+  PEC_DCHECK(issued == consumed);
   if (kStore && lane == 0) bulk_wait_all();
 }
 
@@ -527,6 +533,7 @@ __global__ void crc_final_kernel(const pec_copy_desc* __restrict__ d, int n, Crc
     }
     const uint64_t chunks = (nb + kChunk - 1) >> kCrcLg;
     const uint64_t last_len = nb - ((chunks - 1) << kCrcLg);
+    PEC_DCHECK(last_len > 0 && last_len <= (uint64_t)kChunk);
     const uint32_t r_last = chunk_raw[d[i].first_chunk + chunks - 1];
     const uint32_t r = shift_bytes(k.x2k, entry[i], last_len) ^ r_last;
     entry[i] = ~(r ^ shift_bytes(k.x2k, 0xFFFFFFFFu, nb));

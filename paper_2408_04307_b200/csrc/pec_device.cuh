@@ -6,6 +6,27 @@
 
 #include "pec.h"
 
+// Device-side invariant checks, compiled into the debug library only
+// (libpec_debug.so, -DPEC_DEBUG; _build.build_debug()).  compute-sanitizer
+// is not available on the B200 pool, so out-of-range indices and overruns are
+// caught by these checks plus guard bands around every output buffer
+// (tools/guard_kernels.py).  A failed check prints and traps (the launch
+// then reports an error on the next synchronisation).
+#ifdef PEC_DEBUG
+#include <cstdio>
+#define PEC_DCHECK(cond, ...)                                                    \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      printf("PEC_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);      \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define PEC_DCHECK(cond, ...) \
+  do {                        \
+  } while (0)
+#endif
+
 namespace pecdev {
 
 // SM count of the current device, cached per device id (a pure function of
@@ -38,6 +59,7 @@ __device__ __forceinline__ int find_desc(const pec_copy_desc* __restrict__ d, in
     const int mid = (lo + hi + 1) >> 1;
     if (__ldg(&d[mid].first_chunk) <= ch) lo = mid; else hi = mid - 1;
   }
+  PEC_DCHECK(n > 0 && lo >= 0 && lo < n && __ldg(&d[lo].first_chunk) <= ch);
   return lo;
 }
 
@@ -61,6 +83,7 @@ struct DescCursor {
       }
       ++i;
     }
+    PEC_DCHECK(i >= 0 && i < n && __ldg(&d[i].first_chunk) <= ch);
     return i;
   }
 };

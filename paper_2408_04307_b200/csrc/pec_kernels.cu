@@ -73,6 +73,7 @@ token_hist_kernel(const Id* __restrict__ idx, int L, int64_t n, int E,
     for (int u = 0; u < kHistUnroll; ++u) {
       // ids outside [0, E) (dropped tokens, any width) go to the ignore slot
       const int key = (v[u] >= 0 && v[u] < (Id)E) ? (int)v[u] : E;
+      PEC_DCHECK(key >= 0 && key <= E);
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       if (lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[key], (uint32_t)__popc(peers));
     }
@@ -188,6 +189,7 @@ select_load_aware_kernel(int64_t* __restrict__ counters, int L, int E, int K,
     const unsigned m = __ballot_sync(0xffffffffu, s);
     if (s) {
       const int pos = written + __popc(m & ((1u << lane) - 1u));
+      PEC_DCHECK(pos < K);
       o[pos] = e;
       if (zero_selected) cnt[e] = 0;
     }
@@ -393,6 +395,8 @@ __device__ __forceinline__ Piece piece_of(const pec_copy_desc* __restrict__ d, i
   const uint64_t hi = lo + (1ull << piece_log2);
   const uint64_t end = hi < v.body ? hi : v.body;
   p.bytes = end > lo ? (uint32_t)(end - lo) : 0u;
+  PEC_DCHECK(p.bytes <= (1u << piece_log2) && (p.bytes & 15u) == 0);
+  PEC_DCHECK(v.head + v.body <= v.len);
   p.src = v.s + v.head + lo;
   p.dst = v.t + v.head + lo;
   return p;
@@ -548,6 +552,7 @@ expand_plan_kernel(const pec_plan_template* __restrict__ tmpl, int n,
       const pec_plan_template t = tmpl[i];
       src = t.src_offset;
       nb = t.nbytes;
+      PEC_DCHECK(t.layer < L);
       if (t.layer < 0) {
         keep = true;
       } else if (t.layer < L) {

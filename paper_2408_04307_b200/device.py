@@ -16,7 +16,10 @@ import numpy as np
 
 from .topology import SpecValidationError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpec.so"
+# PEC_LIB=debug loads the build with device-side invariant checks (test
+# tooling, tools/guard_kernels.py); there is no other variant and no fallback
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / (
+    "libpec_debug.so" if os.environ.get("PEC_LIB") == "debug" else "libpec.so")
 ABI_VERSION = 1
 
 PEC_OK = 0

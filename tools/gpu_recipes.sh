@@ -17,7 +17,7 @@ case "$recipe" in
     timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo bench=$?; cat $O/bench.json
     ;;
   launches)   # per-launch list of the bench's kernels (share of the step)
-    CMD="python bench.py --steps 4 --warmup 3 --no-cpu --no-stall"
+    CMD="python bench.py --steps 4 --warmup 3 --no-cpu --no-stall --e2e-steps 5"
     timeout 600 $CMD > $O/plain_launch.log 2>&1 && \
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1; echo ncu=$?
@@ -62,15 +62,13 @@ case "$recipe" in
       -k regex:"pack_crc|crc_fold|crc_final" -s 3 -c 3 -o $O/prof_crc $CMD > $O/ncu_crc.log 2>&1
     echo ncu=$?
     ;;
-  sanitize)   # compute-sanitizer over every libpec kernel (tools/sanitize_kernels.py)
-    K="--kernel-name kns=pack_crc_kernel --kernel-name kns=crc_fold --kernel-name kns=crc_final"
-    K="$K --kernel-name kns=copy_bulk --kernel-name kns=copy_vec --kernel-name kns=token_hist"
-    K="$K --kernel-name kns=select_ --kernel-name kns=expand_plan"
-    for t in memcheck racecheck synccheck initcheck; do
-      timeout 1500 compute-sanitizer --tool $t $K --print-limit 50 \
-        python tools/sanitize_kernels.py > $O/sanitize_$t.txt 2>&1; echo $t=$?
-      tail -3 $O/sanitize_$t.txt
-    done
+  guard)   # bounds evidence without compute-sanitizer (closed on this pool): guard bands
+           # around every output + the debug library's device-side invariant checks
+    PEC_LIB=debug timeout 600 python tools/guard_kernels.py > $O/guard_debug.txt 2>&1; echo guard_debug=$?
+    timeout 600 python tools/guard_kernels.py > $O/guard_release.txt 2>&1; echo guard_release=$?
+    PEC_LIB=debug timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider \
+      > $O/gpu_suite_debug_lib.txt 2>&1; echo suite_debug=$?
+    tail -2 $O/guard_debug.txt $O/guard_release.txt $O/gpu_suite_debug_lib.txt
     ;;
   host_link)   # pinned D2H / push probes
     timeout 300 python tools/d2h_probe.py > $O/d2h_probe.json 2>&1; cat $O/d2h_probe.json

@@ -1,15 +1,25 @@
-"""Drive every libpec kernel once on small inputs, for compute-sanitizer.
+"""Bounds evidence for every libpec kernel without compute-sanitizer.
 
-    compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} \
-        python tools/sanitize_kernels.py
+compute-sanitizer is closed on the B200 pool (runs under it left GPUs
+needing a reset), so out-of-bounds behaviour is checked two ways instead:
+
+* every buffer a kernel writes is allocated with 64 KiB guard bands on both
+  sides filled with a pattern, and the bands are verified after each launch
+  (an overrun or underrun of any output shows up as a changed guard byte);
+* run with PEC_LIB=debug, the library is the build with device-side
+  invariant checks compiled in (PEC_DCHECK: descriptor index in range,
+  chunk inside its descriptor, pipeline counters, selection output slots,
+  TMA piece sizes), which trap on a violation.
+
+    PEC_LIB=debug python tools/guard_kernels.py
 
 Covers token_hist (int32 + int64 ids, dropped ids, cap), both selections
 (pool, reset), the vector and TMA bulk pack/unpack engines (aligned,
-byte-granular and incongruent ranges), device plan expansion +
-pack_indirect, the CRC-computing pack and pec_crc_device (full, partial and
-unaligned chunks, empty entries), and checks every result against the
-oracle, so a clean sanitizer report is also a correct run.  Prints one line
-per kernel family and "sanitize-drive ok" at the end.
+byte-granular and incongruent ranges, ranges ending flush with their
+allocation), device plan expansion + pack_indirect, the CRC-computing pack
+and pec_crc_device (full, partial and unaligned chunks, empty entries), and
+checks every result against the oracle.  Prints one line per kernel family
+and "guard-drive ok" at the end.
 """
 
 from __future__ import annotations
@@ -22,6 +32,33 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
+
+
+GUARD = 64 << 10
+PATTERN = 0xA5
+
+
+def guarded(n, dtype, dev, fill=None):
+    """(full, view): ``view`` has n elements, surrounded by GUARD bytes of
+    PATTERN on both sides inside ``full``."""
+    import torch
+    esize = torch.empty(0, dtype=dtype).element_size()
+    g = GUARD // esize
+    full = torch.empty(n + 2 * g, dtype=dtype, device=dev)
+    full.view(torch.uint8).fill_(PATTERN)
+    view = full[g:g + n]
+    if fill is not None:
+        view.fill_(fill)
+    return full, view
+
+
+def check_guards(full, what: str) -> None:
+    import torch
+    torch.cuda.synchronize()
+    b = full.view(torch.uint8)
+    head, tail = b[:GUARD], b[b.numel() - GUARD:]
+    bad = int((head != PATTERN).sum()) + int((tail != PATTERN).sum())
+    assert bad == 0, f"{what}: {bad} guard bytes overwritten"
 
 
 def main() -> int:
@@ -40,18 +77,23 @@ def main() -> int:
     L, E, n = 3, 16, 5000
     for dtype in (torch.int32, torch.int64):
         ids = torch.from_numpy(rng.integers(-2, E + 3, (L, n))).to(dev, dtype)
-        counts = torch.zeros((2, L, E), dtype=torch.int64, device=dev)
-        delivered = torch.zeros((L, E), dtype=torch.int64, device=dev)
-        scratch = torch.zeros(L * E + 1, dtype=torch.int32, device=dev)
+        cf, counts = guarded(2 * L * E, torch.int64, dev, 0)
+        counts = counts.view(2, L, E)
+        df, delivered = guarded(L * E, torch.int64, dev, 0)
+        delivered = delivered.view(L, E)
+        sf, scratch = guarded(L * E + 1, torch.int32, dev, 0)
         cap = torch.full((L,), 400, dtype=torch.int64, device=dev)
         D.token_hist(ids, counts, scratch, cap=cap, delivered=delivered)
         want = O.route_counts(ids.cpu().numpy(), E, [400] * L)
         assert np.array_equal(counts[0].cpu().numpy(), want)
         assert np.array_equal(delivered.cpu().numpy(), want)
+        for f, w in ((cf, "counters"), (df, "delivered"), (sf, "hist scratch")):
+            check_guards(f, w)
     print("token_hist ok")
 
     # -- selection ------------------------------------------------------------------
-    out = torch.empty((L, 4), dtype=torch.int32, device=dev)
+    of, out = guarded(L * 4, torch.int32, dev)
+    out = out.view(L, 4)
     D.select_sequential(5, L, E, 4, 4, out)
     assert out.cpu().tolist() == [O.select_window(5, m, E, 4, 4) for m in range(L)]
     c = torch.from_numpy(rng.integers(0, 50, (L, E))).to(dev)
@@ -59,22 +101,27 @@ def main() -> int:
     D.select_load_aware(c, 4, out, zero_selected=True)
     snap = out.clone()
     assert out.cpu().tolist() == [O.select_load_aware(host_c[m], 4) for m in range(L)]
-    out2 = torch.empty((L, 2), dtype=torch.int32, device=dev)
+    of2, out2 = guarded(L * 2, torch.int32, dev)
+    out2 = out2.view(L, 2)
     D.select_load_aware(c, 2, out2, pool=snap)
+    check_guards(of, "selection")
+    check_guards(of2, "pooled selection")
     print("selection ok")
 
     # -- pack / unpack engines -------------------------------------------------------
     size = 6 << 20
-    state = torch.randint(0, 256, (size,), dtype=torch.uint8, device=dev)
+    stf, state = guarded(size, torch.uint8, dev)
+    state.copy_(torch.randint(0, 256, (size,), dtype=torch.uint8, device=dev))
     host = state.cpu().numpy()
     for congruent in (True, False):
         copies, pos = [], 0
-        for ln in [0, 1, 15, 17, 4095, 32768, 32769, 100_003, 1 << 20]:
-            src = int(rng.integers(0, size - ln))
+        for j, ln in enumerate([0, 1, 15, 17, 4095, 32768, 32769, 100_003, 1 << 20, 77_777]):
+            # the last range ends flush with the end of the state view
+            src = size - ln if j == 9 else int(rng.integers(0, size - ln))
             dst = pos + ((src - pos) % 256) if congruent else pos + int(rng.integers(0, 64))
             copies.append((src, dst, ln))
             pos = dst + ln
-        staging = torch.zeros(pos + 64, dtype=torch.uint8, device=dev)
+        sgf, staging = guarded(pos + 64, torch.uint8, dev, 0)
         table = np.zeros(len(copies), dtype=D.DESC_DTYPE)
         for i, (s, t, m) in enumerate(copies):
             table[i] = (state.data_ptr() + s, staging.data_ptr() + t, m, 0)
@@ -85,18 +132,22 @@ def main() -> int:
             staging.zero_()
             D.pack(dt, len(copies), total, 15, mode)
             assert np.array_equal(staging.cpu().numpy(), want), (congruent, mode)
-        chunk = torch.empty(D.crc_scratch_words(total), dtype=torch.int32, device=dev)
-        entry = torch.empty(len(copies), dtype=torch.int32, device=dev)
+            check_guards(sgf, f"staging (mode {mode})")
+        cgf, chunk = guarded(D.crc_scratch_words(total), torch.int32, dev)
+        egf, entry = guarded(len(copies), torch.int32, dev)
         staging.zero_()
         D.pack_crc(dt, len(copies), total, chunk, entry)
         assert np.array_equal(staging.cpu().numpy(), want)
+        for f, w in ((sgf, "staging (crc)"), (cgf, "chunk crc"), (egf, "entry crc")):
+            check_guards(f, w)
         got = entry.cpu().numpy().view(np.uint32)
         for (s, _, m), cval in zip(copies, got):
             assert int(cval) == O.crc32c(host[s:s + m])
         D.crc_device(dt, len(copies), total, chunk, entry)
         assert np.array_equal(entry.cpu().numpy().view(np.uint32), got)
+        check_guards(stf, "state (crc_device must not write)")
         # unpack: staging -> a wiped copy of the state
-        back = torch.zeros_like(state)
+        bgf, back = guarded(size, torch.uint8, dev, 0)
         rt = np.zeros(len(copies), dtype=D.DESC_DTYPE)
         for i, (s, t, m) in enumerate(copies):
             rt[i] = (staging.data_ptr() + t, back.data_ptr() + s, m, 0)
@@ -106,6 +157,7 @@ def main() -> int:
         bh = back.cpu().numpy()
         for s, _, m in copies:
             assert np.array_equal(bh[s:s + m], host[s:s + m])
+        check_guards(bgf, "unpack target")
     print("pack/unpack/pack_crc/crc_device ok")
 
     # -- device plan expansion + indirect pack ---------------------------------------
@@ -114,9 +166,9 @@ def main() -> int:
     arena = StateArena(layout, [1], dev)
     hs = arena.buffer.cpu().numpy()
     tmpl = PlanTemplate(layout, arena, 1, "equal_pec", dev)
-    staging = torch.zeros(tmpl.max_bytes + 512, dtype=torch.uint8, device=dev)
-    table = torch.empty(max(1, tmpl.n) * 4, dtype=torch.int64, device=dev)
-    totals = torch.zeros(2, dtype=torch.int64, device=dev)
+    sgf, staging = guarded(tmpl.max_bytes + 512, torch.uint8, dev, 0)
+    tgf, table = guarded(max(1, tmpl.n) * 4, torch.int64, dev)
+    ogf, totals = guarded(2, torch.int64, dev, 0)
     sel = np.stack([np.sort(rng.choice(8, size=3, replace=False)) for _ in range(3)])
     sel_d = torch.from_numpy(sel.astype(np.int32)).to(dev)
     D.expand_plan(tmpl.tensor, tmpl.n, sel_d, arena.base_address, staging.data_ptr(), table,
@@ -126,12 +178,14 @@ def main() -> int:
     st = StagingLayout.build(build_phase_assignment(layout, due, "equal_pec").get(1, ()), arena, 1)
     copies = [(e.src_offset, e.stage_offset, e.nbytes) for e in st.entries]
     assert np.array_equal(staging.cpu().numpy(), O.pack(hs, copies, tmpl.max_bytes + 512))
-    chunk = torch.empty(D.crc_scratch_words(tmpl.max_chunks()), dtype=torch.int32, device=dev)
-    entry = torch.empty(tmpl.n, dtype=torch.int32, device=dev)
+    cgf, chunk = guarded(D.crc_scratch_words(tmpl.max_chunks()), torch.int32, dev)
+    egf, entry = guarded(tmpl.n, torch.int32, dev)
     D.pack_crc(table, tmpl.n, tmpl.max_chunks(), chunk, entry, totals_dev=totals)
-    torch.cuda.synchronize()
+    for f, w in ((sgf, "plan staging"), (tgf, "expanded table"), (ogf, "totals"),
+                 (cgf, "chunk crc (indirect)"), (egf, "entry crc (indirect)")):
+        check_guards(f, w)
     print("expand_plan/pack_indirect ok")
-    print("sanitize-drive ok")
+    print(f"guard-drive ok (library: {D.LIB_PATH.name})")
     return 0
 
 
