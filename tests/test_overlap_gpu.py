@@ -177,6 +177,14 @@ def test_snapshots_stay_exact_when_a_stream_lags(dev, tmp_path, selection, lag):
 @pytest.mark.parametrize("lag,drop", [("pack", "wait_pack"), ("compute", "stream_wait")])
 @pytest.mark.parametrize("selection", ["sequential", "load_aware"])
 def test_negative_controls_detect_a_torn_snapshot(dev, tmp_path, selection, lag, drop):
-    mismatches, checked = _run(dev, tmp_path, selection, 3, lag=lag, drop=drop)
+    """Either the bytes differ from the fingerprint, or — device-planned
+    snapshots whose expansion raced the selection it depends on — the
+    engine's check of every expanded row against the host plan refuses the
+    snapshot (snapshot.finalize_pending)."""
+    try:
+        mismatches, checked = _run(dev, tmp_path, selection, 3, lag=lag, drop=drop)
+    except RuntimeError as exc:
+        assert selection == "load_aware" and "disagrees with the host plan" in str(exc), exc
+        return
     assert checked > 50
     assert mismatches, f"dropping {drop} was not detected"
