@@ -44,7 +44,7 @@ constexpr int kHistThreads = 256;
 constexpr int kHistUnroll = 8;
 
 template <typename Id>
-__global__ void __launch_bounds__(kHistThreads)
+__global__ void __launch_bounds__(kHistThreads, 1)
 token_hist_kernel(const Id* __restrict__ idx, int L, int64_t n, int E,
                   const int64_t* __restrict__ cap, int64_t* __restrict__ counters,
                   int tiers, int64_t* __restrict__ delivered,
