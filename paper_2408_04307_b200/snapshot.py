@@ -153,6 +153,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
         self._persist: Dict[int, Tuple[Future, List[StoreEntry]]] = {}
         self._abort_persist = threading.Event()
         self._pending_bid: Optional[int] = None  # device-planned snapshot awaiting its drain
+        self._pinned_cache: Dict[tuple, object] = {}
         self.stats = {"pack_ms": [], "drain_ms": [], "persist_s": [], "snap_bytes": []}
 
     # -- buffers -----------------------------------------------------------------
@@ -191,6 +192,21 @@ class DeviceCheckpointEngine(CheckpointEngine):
                 self._shared[buffer_id] = shb
                 self.host[buffer_id] = shb.tensor
         return self.host[buffer_id]
+
+    def _pinned(self, tag, buffer_id: int, n: int, dtype):
+        """A pinned host array of >= n elements owned by (tag, buffer_id),
+        allocated once and reused by every later snapshot into that buffer:
+        pinning inside a checkpoint would stall the host between the launches
+        it enqueues.  Safe to reuse: a buffer's small host-side records (CRCs,
+        sizes, selections) are read before the buffer can be snapshotted
+        into again (the state machine frees it only after its persist)."""
+        import torch
+        key = (tag, buffer_id)
+        t = self._pinned_cache.get(key)
+        if t is None or t.numel() < n or t.dtype != dtype:
+            t = torch.empty(max(1, n), dtype=dtype, pin_memory=True)
+            self._pinned_cache[key] = t
+        return t[:n]
 
     # -- node-shared snapshot metadata (cross-process memory restore) ---------------
     def _meta_path(self, rank: int, buffer_id: int) -> str:
@@ -395,7 +411,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
             if crc_mode:
                 rec.crc_segments = []
                 rec.crc_keys = [e.store_key for r in self.ranks for e in layouts[r].entries]
-            for sub, lo, hi in table.segments:
+            for si, (sub, lo, hi) in enumerate(table.segments):
                 self._launch_pack(sub, ps)
                 seg_done = torch.cuda.Event()
                 seg_done.record(ps)
@@ -406,7 +422,8 @@ class DeviceCheckpointEngine(CheckpointEngine):
                 with torch.cuda.stream(cs):
                     self._drain_range(host, lo, min(hi, nbytes))
                     if crc_mode and sub.n:
-                        pinned = torch.empty(sub.n, dtype=torch.int32, pin_memory=True)
+                        pinned = self._pinned(("seg_crc", id(table), si), buf.buffer_id, sub.n,
+                                              torch.int32)
                         pinned.copy_(sub.entry_crc[:sub.n], non_blocking=True)
                         rec.crc_segments.append((pinned, sub.rows, sub.row_bytes))
             rec.pack_done.record(ps)
@@ -422,7 +439,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
             if table.segments is None:
                 self._drain(host, nbytes)
             if self.pack_mode == D.MODE_CRC and table.n and table.segments is None:
-                rec.entry_crc = torch.empty(table.n, dtype=torch.int32, pin_memory=True)
+                rec.entry_crc = self._pinned("entry_crc", buf.buffer_id, table.n, torch.int32)
                 rec.entry_crc.copy_(table.entry_crc[:table.n], non_blocking=True)
                 rec.crc_keys = [e.store_key for r in self.ranks for e in layouts[r].entries]
         rec.drain_done.record(cs)
@@ -525,8 +542,8 @@ class DeviceCheckpointEngine(CheckpointEngine):
         ms.wait_event(expanded)
         R = len(self.ranks)
         head = 2 * R
-        meta = torch.empty(head + snap_sel_dev.numel() + persist_sel_dev.numel(),
-                           dtype=torch.int64, pin_memory=True)
+        meta = self._pinned("meta", buf.buffer_id,
+                            head + snap_sel_dev.numel() + persist_sel_dev.numel(), torch.int64)
         with torch.cuda.stream(ms):
             for i, r in enumerate(self.ranks):
                 meta[2 * i:2 * i + 2].copy_(self._dev_totals_r[r], non_blocking=True)
@@ -536,8 +553,8 @@ class DeviceCheckpointEngine(CheckpointEngine):
                                                      non_blocking=True)
             # the expanded tables themselves: finalize_pending checks every
             # kept row's staging offset and length against the host plan
-            tabs = torch.empty(sum(4 * self.templates[r].n for r in self.ranks),
-                               dtype=torch.int64, pin_memory=True)
+            tabs = self._pinned("tabs", buf.buffer_id,
+                                sum(4 * self.templates[r].n for r in self.ranks), torch.int64)
             o = 0
             for r in self.ranks:
                 n4 = 4 * self.templates[r].n
@@ -628,7 +645,7 @@ class DeviceCheckpointEngine(CheckpointEngine):
                 # template order per rank; dropped entries carry nbytes 0 (crc 0)
                 total_n = sum(t.n for t in self.templates.values())
                 if total_n:
-                    rec.entry_crc = torch.empty(total_n, dtype=torch.int32, pin_memory=True)
+                    rec.entry_crc = self._pinned("entry_crc", bid, total_n, torch.int32)
                     o, keys = 0, []
                     for r in self.ranks:
                         t = self.templates[r]
