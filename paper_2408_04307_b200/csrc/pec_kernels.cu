@@ -5,7 +5,7 @@
 //                            router ids, capacity clamp, int64 accumulation
 //                            (reference: simulator.py:88-95, :560-567)
 //   select_sequential_kernel window selection (selector.py:21-32)
-//   select_load_aware_kernel top-K by (-unsaved, id) + mark_saved
+//   select_load_aware_kernel top-K by (-unsaved, id) + mark_saved (block radix sort)
 //                            (selector.py:86-100, simulator.py:339-354)
 //   copy_vec_kernel          gather/scatter engine, LDG/STG.128
 //   copy_bulk_kernel         gather/scatter engine, TMA bulk (cp.async.bulk)
@@ -16,6 +16,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <climits>
+
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "pec.h"
@@ -134,68 +138,88 @@ __global__ void select_sequential_kernel(int64_t c, int L, int E, int width, int
   }
 }
 
-// One warp per layer.  Candidate e is selected iff fewer than K candidates
-// beat it under (count desc, id asc).  A per-warp shared bitmap over expert
-// ids turns the selection into an ascending compaction (ballot + popc).
-constexpr int kSelWarps = 4;
+// One CTA per layer.  Candidates are all E experts, or the valid distinct ids
+// of the layer's pool (a shared bitmap drops duplicates and ids outside
+// [0, E)).  A block radix sort of (count, id) pairs — descending by count and
+// stable, over ids in ascending order — leaves ties in ascending id order, so
+// ranks 0..K-1 are the top-K by (count desc, id asc); they are flagged in the
+// bitmap and compacted in ascending id order with a block scan, and their
+// counters reset when asked.  O(E log E) per layer: 4096 experts cost one
+// 16-item-per-thread sort (the round-1 kernel compared every candidate with
+// every other, O(E^2) per lane).
+constexpr int kSelThreads = 256;
 
-__global__ void __launch_bounds__(32 * kSelWarps)
-select_load_aware_kernel(int64_t* __restrict__ counters, int L, int E, int K,
+template <int kItems>
+__global__ void __launch_bounds__(kSelThreads)
+select_load_aware_kernel(int64_t* __restrict__ counters, int E, int K,
                          const int32_t* __restrict__ pool, int P,
                          int32_t* __restrict__ out, int zero_selected) {
-  extern __shared__ uint8_t sel_bits[];  // kSelWarps * E
-  const int warp_in_block = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int layer = blockIdx.x * kSelWarps + warp_in_block;
-  if (layer >= L) return;  // warp-uniform
-  uint8_t* bits = sel_bits + (int64_t)warp_in_block * E;
+  using Sort = cub::BlockRadixSort<long long, kSelThreads, kItems, int>;
+  using Scan = cub::BlockScan<int, kSelThreads>;
+  using Sum = cub::BlockReduce<int, kSelThreads>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+    typename Sum::TempStorage sum;
+  } tmp;
+  __shared__ uint8_t flag[kSelThreads * kItems];   // candidate, then selected
+  __shared__ int n_cand;
+  const int tid = threadIdx.x, layer = blockIdx.x;
   int64_t* cnt = counters + (int64_t)layer * E;
-  const int32_t* pl = pool ? pool + (int64_t)layer * P : nullptr;
-  const int ncand = pool ? P : E;
-
-  for (int e = lane; e < E; e += 32) bits[e] = 0;
-  __syncwarp();
-
-  int nvalid = 0;  // valid candidates in the pool (all lanes agree)
-  for (int i = 0; i < ncand; ++i) {
-    const int e = pl ? pl[i] : i;
-    nvalid += (e >= 0 && e < E);
+  for (int e = tid; e < kSelThreads * kItems; e += kSelThreads)
+    flag[e] = (pool == nullptr && e < E) ? 1 : 0;
+  __syncthreads();
+  if (pool != nullptr) {
+    for (int i = tid; i < P; i += kSelThreads) {
+      const int e = pool[(int64_t)layer * P + i];
+      if (e >= 0 && e < E) flag[e] = 1;
+    }
+    __syncthreads();
   }
-  const int kk = K < nvalid ? K : nvalid;
-
-  for (int i0 = 0; i0 < ncand; i0 += 32) {
-    const int i = i0 + lane;
-    int e = -1;
-    if (i < ncand) e = pl ? pl[i] : i;
-    if (e >= 0 && e < E) {
-      const int64_t ce = cnt[e];
-      int rank = 0;
-      for (int j = 0; j < ncand && rank < kk; ++j) {
-        const int ej = pl ? pl[j] : j;
-        if (ej < 0 || ej >= E) continue;
-        const int64_t cj = cnt[ej];
-        rank += (cj > ce) || (cj == ce && ej < e);
-      }
-      if (rank < kk) bits[e] = 1;
+  long long key[kItems];
+  int id[kItems];
+  int mine = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int e = tid * kItems + j;               // blocked: ascending ids in input order
+    const bool cand = e < E && flag[e];
+    key[j] = cand ? (long long)cnt[e] : LLONG_MIN;
+    id[j] = cand ? e : -1;
+    mine += cand;
+  }
+  const int total = Sum(tmp.sum).Sum(mine);
+  if (tid == 0) n_cand = total;
+  __syncthreads();
+  Sort(tmp.sort).SortDescending(key, id);         // stable: ties keep ascending id order
+  __syncthreads();
+  const int kk = K < n_cand ? K : n_cand;
+  for (int e = tid; e < kSelThreads * kItems; e += kSelThreads) flag[e] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int rank = tid * kItems + j;
+    if (rank < kk) {
+      PEC_DCHECK(id[j] >= 0 && id[j] < E);
+      flag[id[j]] = 1;
     }
   }
-  __syncwarp();
-
+  __syncthreads();
+  int mark = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) mark += flag[tid * kItems + j];
+  int pos = 0;
+  Scan(tmp.scan).ExclusiveSum(mark, pos);
   int32_t* o = out + (int64_t)layer * K;
-  int written = 0;
-  for (int e0 = 0; e0 < E; e0 += 32) {
-    const int e = e0 + lane;
-    const bool s = e < E && bits[e];
-    const unsigned m = __ballot_sync(0xffffffffu, s);
-    if (s) {
-      const int pos = written + __popc(m & ((1u << lane) - 1u));
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int e = tid * kItems + j;
+    if (flag[e]) {
       PEC_DCHECK(pos < K);
-      o[pos] = e;
+      o[pos++] = e;
       if (zero_selected) cnt[e] = 0;
     }
-    written += __popc(m);
   }
-  for (int j = written + lane; j < K; j += 32) o[j] = -1;
+  for (int j = kk + tid; j < K; j += kSelThreads) o[j] = -1;
 }
 
 // ------------------------------------------------------------------------
@@ -764,10 +788,17 @@ int pec_select_load_aware(int64_t* counters, int L, int E, int K,
   if (L < 1 || E < 1 || K < 1 || counters == nullptr || out == nullptr) return PEC_E_INVAL;
   if (pool != nullptr && P < 0) return PEC_E_INVAL;
   if (E > kMaxExperts) return PEC_E_RANGE;
-  const int blocks = (L + kSelWarps - 1) / kSelWarps;
-  const size_t smem = (size_t)kSelWarps * E;
-  select_load_aware_kernel<<<blocks, 32 * kSelWarps, smem, as_stream(stream)>>>(
-      counters, L, E, K, pool, pool ? P : 0, out, zero_selected);
+  cudaStream_t st = as_stream(stream);
+  const int p = pool ? P : 0;
+  if (E <= kSelThreads)
+    select_load_aware_kernel<1><<<L, kSelThreads, 0, st>>>(counters, E, K, pool, p, out,
+                                                           zero_selected);
+  else if (E <= kSelThreads * 4)
+    select_load_aware_kernel<4><<<L, kSelThreads, 0, st>>>(counters, E, K, pool, p, out,
+                                                           zero_selected);
+  else
+    select_load_aware_kernel<16><<<L, kSelThreads, 0, st>>>(counters, E, K, pool, p, out,
+                                                            zero_selected);
   return launch_status();
 }
 

@@ -135,6 +135,32 @@ def test_select_load_aware_ties_pools_and_reset(dev, E):
         assert np.array_equal(dp.cpu().numpy(), pers_after)
 
 
+@pytest.mark.parametrize("E", [8, 300, 4096])
+def test_select_load_aware_pools_with_duplicates_and_invalid_ids(dev, E):
+    """Pool entries may repeat or fall outside [0, E) (padding -1 of a
+    shorter selection): the candidates are the distinct valid ids, exactly
+    as the reference's pool semantics (selector.py:91-100, oracle)."""
+    import torch
+    from paper_2408_04307_b200 import device as D
+    rng = np.random.default_rng(E + 7)
+    L, P = 4, 24
+    counts = rng.integers(0, 5, size=(L, E)).astype(np.int64)
+    pool = rng.integers(-3, E + 3, size=(L, P)).astype(np.int32)
+    pool[:, 1] = pool[:, 0]                       # a duplicate in every row
+    for k in (1, 3, P):
+        out = torch.empty((L, k), dtype=torch.int32, device=dev)
+        dc = torch.from_numpy(counts).to(dev)
+        D.select_load_aware(dc, k, out, pool=torch.from_numpy(pool).to(dev), zero_selected=True)
+        got = out.cpu().tolist()
+        after = counts.copy()
+        for m in range(L):
+            want = O.select_load_aware(counts[m], k, pool=pool[m].tolist())
+            assert [e for e in got[m] if e >= 0] == want, (m, k)
+            assert got[m][len(want):] == [-1] * (k - len(want))
+            after[m, want] = 0
+        assert np.array_equal(dc.cpu().numpy(), after)
+
+
 def test_select_load_aware_golden(dev):
     import json
     import torch
