@@ -411,11 +411,16 @@ class DeviceCheckpointEngine(CheckpointEngine):
             if crc_mode:
                 rec.crc_segments = []
                 rec.crc_keys = [e.store_key for r in self.ranks for e in layouts[r].entries]
-            for si, (sub, lo, hi) in enumerate(table.segments):
+            # every segment's pack first, back to back on the pack stream (the
+            # host enqueues the drains while the GPU packs), then each
+            # segment's drain behind its own event on the copy stream
+            seg_done = []
+            for sub, _, _ in table.segments:
                 self._launch_pack(sub, ps)
-                seg_done = torch.cuda.Event()
-                seg_done.record(ps)
-                cs.wait_event(seg_done)
+                seg_done.append(torch.cuda.Event())
+                seg_done[-1].record(ps)
+            for si, (sub, lo, hi) in enumerate(table.segments):
+                cs.wait_event(seg_done[si])
                 if rec.drain_start is None:
                     rec.drain_start = torch.cuda.Event(enable_timing=True)
                     rec.drain_start.record(cs)
