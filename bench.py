@@ -496,11 +496,12 @@ class Retention:
 
 def measure_host_link(eng, world, dev):
     """Host-link roofline measured in this run, on the drain's own path (the
-    copy stream, 256 MiB pieces): 1 GiB pinned D2H, best of 5, each rank
-    alone in turn, then all ranks started together (per-trial max over
-    ranks).  With one GPU the two are the same measurement."""
+    copy stream, 256 MiB pieces): 4 GiB pinned D2H (or the whole staging
+    buffer if smaller), best of 5, each rank alone in turn, then all ranks
+    started together (per-trial max over ranks).  With one GPU the two are
+    the same measurement."""
     import torch
-    n = min(1 << 30, eng.staging.numel(), eng.host[0].numel())
+    n = min(4 << 30, eng.staging.numel(), eng.host[0].numel())
     eng.host[0][:n].copy_(eng.staging[:n])  # first touch of the pinned pages
     rank = int(os.environ.get("RANK", 0))
 
@@ -872,7 +873,7 @@ def run_b200(args):
         e2e["frac_of_host_link"] = round(e2e["per_gpu"] / link_ref, 4)
         host_link = {"achieved": round(drain_gbs, 2), "peak": round(link_alone, 2),
                      "unit": "GB/s",
-                     "peak_kind": "measured in this run: 1 GiB pinned D2H in the drain's "
+                     "peak_kind": "measured in this run: 4 GiB pinned D2H in the drain's "
                                   "256 MiB pieces on its copy stream, best of 5, this GPU alone",
                      "peak_all_gpus_concurrent": round(link_conc, 2),
                      "frac": round(drain_gbs / link_alone, 4),
