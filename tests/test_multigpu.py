@@ -37,3 +37,23 @@ def test_multirank_selection_persist_and_recover(dev):
     assert len(lines) == n
     for r in lines:
         assert r["selection_ok"] and r["files_ok"] and r["restore_ok"] and r["counters_ok"], r
+
+
+def test_config3_dp8_as_fewer_processes_over_nccl(dev):
+    """BASELINE config 3 itself (dp=8 x ep=8 on two 4-GPU nodes) with every
+    process hosting 8 / n_gpus ranks in one engine, over NCCL: the same
+    checks, eight writers per version."""
+    import torch
+    n = min(torch.cuda.device_count(), 4)
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           str(ROOT / "tools" / "multirank_gpu.py"), "--config3", "--ranks-per-proc", str(8 // n)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    lines = [json.loads(ln) for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    assert len(lines) == n
+    for r in lines:
+        assert r["layout_ranks"] == 8 and r["writers"] == 8, r
+        assert r["selection_ok"] and r["files_ok"] and r["restore_ok"] and r["counters_ok"], r
