@@ -876,8 +876,9 @@ def run_b200(args):
                      "peak_kind": "measured in this run: 4 GiB pinned D2H in the drain's "
                                   "256 MiB pieces on its copy stream, best of 5, this GPU alone",
                      "peak_all_gpus_concurrent": round(link_conc, 2),
-                     "frac": round(drain_gbs / link_alone, 4),
-                     "frac_of_concurrent": round(drain_gbs / link_conc, 4)}
+                     # this rank's drain vs the link alone; the whole-job rate against
+                     # the all-ranks-at-once peak is e2e.frac_of_host_link
+                     "frac": round(drain_gbs / link_alone, 4)}
 
         # ---- persist probe: one version, this run's persist rate --------------
         if store is not None:
