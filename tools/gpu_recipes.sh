@@ -41,7 +41,7 @@ case "$recipe" in
     CMD="python bench.py --workload gpt125m --steps 3 --warmup 3 --no-cpu --no-stall --no-e2e"
     timeout 600 $CMD > $O/plain_la.log 2>&1 && \
       timeout 900 ncu --set full --clock-control none --import-source on \
-        -k regex:"token_hist|select_load|expand_plan|copy_bulk" -s 8 -c 5 \
+        -k regex:"token_hist|select_load|expand_plan|copy_bulk|pack_crc|crc_fold|crc_final" -s 8 -c 8 \
         -o $O/prof_loadaware $CMD > $O/ncu_la.log 2>&1; echo ncu=$?
     ;;
   profile_crc)   # the CRC-computing pack (GPT-MoE 350M-16E)
