@@ -62,7 +62,11 @@ def check_guards(full, what: str) -> None:
 
 
 def main() -> int:
+    import os
     import torch
+    from paper_2408_04307_b200 import _build
+    if os.environ.get("PEC_LIB") == "debug":
+        _build.build_debug()          # (re)built in place when missing or stale
     from conftest import make_layout
     from oracle import pec_oracle as O
     from paper_2408_04307_b200 import build_phase_assignment
