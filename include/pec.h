@@ -86,7 +86,8 @@ int pec_select_sequential(int64_t c, int L, int E, int width, int stride,
  *   (selector.py:86-88) as used by Simulation._selections / _trigger_checkpoint
  *   (simulator.py:339-354, :425-432).
  * Per layer: the min(K, |pool|) candidates with the largest counters
- * [L][E] int64, ties to the lowest expert id; written sorted ascending into
+ * [L][E] int64 (token counts, >= 0), ties to the lowest expert id; pool
+ * duplicates count once; written sorted ascending into
  * out [L][K] (unused slots = -1).  pool [L][P] int32 restricts candidates
  * (entries outside [0,E) are skipped), or NULL for all E experts.  With
  * zero_selected != 0 the selected counters are reset to 0 in place. */

@@ -140,60 +140,66 @@ __global__ void select_sequential_kernel(int64_t c, int L, int E, int width, int
 
 // One CTA per layer.  Candidates are all E experts, or the valid distinct ids
 // of the layer's pool (a shared bitmap drops duplicates and ids outside
-// [0, E)).  A block radix sort of (count, id) pairs — descending by count and
-// stable, over ids in ascending order — leaves ties in ascending id order, so
-// ranks 0..K-1 are the top-K by (count desc, id asc); they are flagged in the
-// bitmap and compacted in ascending id order with a block scan, and their
-// counters reset when asked.  O(E log E) per layer: 4096 experts cost one
-// 16-item-per-thread sort (the round-1 kernel compared every candidate with
-// every other, O(E^2) per lane).
-constexpr int kSelThreads = 256;
-
-template <int kItems>
-__global__ void __launch_bounds__(kSelThreads)
+// [0, E)).  A block radix sort of (count + 1, id) pairs — descending and
+// stable, over ids in ascending order, non-candidates keyed 0 so they sort
+// last — leaves ties in ascending id order, so ranks 0..K-1 are the top-K by
+// (count desc, id asc); they are flagged in the bitmap and compacted in
+// ascending id order with a block scan, and their counters reset when asked.
+// The sort only visits the bits the layer's largest key uses (a block max
+// first), and the CTA is one warp for E <= 32.  O(E log E) per layer: 4096
+// experts cost one 16-item-per-thread sort (round 1 compared every candidate
+// with every other, O(E^2) per lane).
+template <int kThreads, int kItems>
+__global__ void __launch_bounds__(kThreads)
 select_load_aware_kernel(int64_t* __restrict__ counters, int E, int K,
                          const int32_t* __restrict__ pool, int P,
                          int32_t* __restrict__ out, int zero_selected) {
-  using Sort = cub::BlockRadixSort<long long, kSelThreads, kItems, int>;
-  using Scan = cub::BlockScan<int, kSelThreads>;
-  using Sum = cub::BlockReduce<int, kSelThreads>;
+  using Sort = cub::BlockRadixSort<unsigned long long, kThreads, kItems, int>;
+  using Scan = cub::BlockScan<int, kThreads>;
+  using Max = cub::BlockReduce<unsigned long long, kThreads>;
   __shared__ union {
     typename Sort::TempStorage sort;
     typename Scan::TempStorage scan;
-    typename Sum::TempStorage sum;
+    typename Max::TempStorage max;
   } tmp;
-  __shared__ uint8_t flag[kSelThreads * kItems];   // candidate, then selected
+  __shared__ uint8_t flag[kThreads * kItems];   // candidate, then selected
   __shared__ int n_cand;
+  __shared__ int end_bit;
   const int tid = threadIdx.x, layer = blockIdx.x;
   int64_t* cnt = counters + (int64_t)layer * E;
-  for (int e = tid; e < kSelThreads * kItems; e += kSelThreads)
+  for (int e = tid; e < kThreads * kItems; e += kThreads)
     flag[e] = (pool == nullptr && e < E) ? 1 : 0;
+  if (tid == 0) n_cand = 0;
   __syncthreads();
   if (pool != nullptr) {
-    for (int i = tid; i < P; i += kSelThreads) {
+    for (int i = tid; i < P; i += kThreads) {
       const int e = pool[(int64_t)layer * P + i];
       if (e >= 0 && e < E) flag[e] = 1;
     }
     __syncthreads();
   }
-  long long key[kItems];
+  unsigned long long key[kItems];
   int id[kItems];
   int mine = 0;
+  unsigned long long kmax = 0;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const int e = tid * kItems + j;               // blocked: ascending ids in input order
     const bool cand = e < E && flag[e];
-    key[j] = cand ? (long long)cnt[e] : LLONG_MIN;
+    // counters are token counts (>= 0): count + 1 keeps every candidate above 0
+    key[j] = cand ? (unsigned long long)cnt[e] + 1ull : 0ull;
     id[j] = cand ? e : -1;
     mine += cand;
+    kmax = key[j] > kmax ? key[j] : kmax;
   }
-  const int total = Sum(tmp.sum).Sum(mine);
-  if (tid == 0) n_cand = total;
+  if (mine) atomicAdd(&n_cand, mine);
+  const unsigned long long bmax = Max(tmp.max).Reduce(kmax, cub::Max());
+  if (tid == 0) end_bit = bmax ? 64 - __clzll((long long)bmax) : 1;
   __syncthreads();
-  Sort(tmp.sort).SortDescending(key, id);         // stable: ties keep ascending id order
+  Sort(tmp.sort).SortDescending(key, id, 0, end_bit);   // stable: ties keep id order
   __syncthreads();
   const int kk = K < n_cand ? K : n_cand;
-  for (int e = tid; e < kSelThreads * kItems; e += kSelThreads) flag[e] = 0;
+  for (int e = tid; e < kThreads * kItems; e += kThreads) flag[e] = 0;
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
@@ -219,7 +225,7 @@ select_load_aware_kernel(int64_t* __restrict__ counters, int E, int K,
       if (zero_selected) cnt[e] = 0;
     }
   }
-  for (int j = kk + tid; j < K; j += kSelThreads) o[j] = -1;
+  for (int j = kk + tid; j < K; j += kThreads) o[j] = -1;
 }
 
 // ------------------------------------------------------------------------
@@ -790,15 +796,18 @@ int pec_select_load_aware(int64_t* counters, int L, int E, int K,
   if (E > kMaxExperts) return PEC_E_RANGE;
   cudaStream_t st = as_stream(stream);
   const int p = pool ? P : 0;
-  if (E <= kSelThreads)
-    select_load_aware_kernel<1><<<L, kSelThreads, 0, st>>>(counters, E, K, pool, p, out,
-                                                           zero_selected);
-  else if (E <= kSelThreads * 4)
-    select_load_aware_kernel<4><<<L, kSelThreads, 0, st>>>(counters, E, K, pool, p, out,
-                                                           zero_selected);
+  if (E <= 32)
+    select_load_aware_kernel<32, 1><<<L, 32, 0, st>>>(counters, E, K, pool, p, out,
+                                                      zero_selected);
+  else if (E <= 256)
+    select_load_aware_kernel<256, 1><<<L, 256, 0, st>>>(counters, E, K, pool, p, out,
+                                                        zero_selected);
+  else if (E <= 1024)
+    select_load_aware_kernel<256, 4><<<L, 256, 0, st>>>(counters, E, K, pool, p, out,
+                                                        zero_selected);
   else
-    select_load_aware_kernel<16><<<L, kSelThreads, 0, st>>>(counters, E, K, pool, p, out,
-                                                            zero_selected);
+    select_load_aware_kernel<256, 16><<<L, 256, 0, st>>>(counters, E, K, pool, p, out,
+                                                         zero_selected);
   return launch_status();
 }
 
