@@ -64,34 +64,91 @@ constexpr int kWarps = 8;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kRing = 4;                        // stages per warp
 
-struct CrcConsts {
-  uint32_t x2k[64];         // x^(2^k) mod P
-  uint32_t y;               // x^4096: one chain step (512 bytes)
-};
-
-__host__ __device__ __forceinline__ uint32_t gf2_mul(uint32_t a, uint32_t b) {
+__host__ __device__ constexpr uint32_t gf2_mul(uint32_t a, uint32_t b) {
   uint32_t p = 0;
-#pragma unroll 8
   for (int i = 31; i >= 0; --i) {
-    p ^= b & (0u - ((a >> i) & 1u));
-    b = (b >> 1) ^ (kPoly & (0u - (b & 1u)));
+    if ((a >> i) & 1u) p ^= b;
+    b = (b & 1u) ? (b >> 1) ^ kPoly : b >> 1;
   }
   return p;
 }
 
-__device__ __forceinline__ uint32_t xpow_bits(const uint32_t* x2k, uint64_t nbits) {
+// x^nbits mod P from the x^(2^k) table
+__host__ __device__ constexpr uint32_t xpow_bits(const uint32_t* x2k, uint64_t nbits) {
   uint32_t acc = 1u << 31;  // 1
-  int k = 0;
-  while (nbits) {
+  for (int k = 0; nbits; nbits >>= 1, ++k)
     if (nbits & 1u) acc = gf2_mul(x2k[k], acc);
-    nbits >>= 1;
-    ++k;
-  }
   return acc;
 }
 
-__device__ __forceinline__ uint32_t shift_bytes(const uint32_t* x2k, uint32_t r, uint64_t n) {
-  return n ? gf2_mul(xpow_bits(x2k, n << 3), r) : r;
+// Every constant the CRC kernels use, computed by the compiler (constexpr)
+// and stored in the device image: the kernels copy what they need into
+// shared memory instead of deriving it with thousands of GF(2) products per
+// launch (round-1/early round-2 kernels built them per CTA).
+struct CrcTables {
+  uint32_t x2k[64];             // x^(2^k) mod P
+  uint32_t ybase[4][256];       // slicing-by-4 tables of Y = x^4096: T_k[e] = Y * (e << 8k)
+  uint32_t lanetab[8 * 16 * 32];  // lane l's 4-bit windows of x^(128 (31 - l)), [p][v][l]
+  uint32_t nib4[4][128];        // 4-bit windows of x^(32 (4 - t)), t = 0..3
+  uint32_t t8[256];             // the standard byte table (partial chunks)
+  uint32_t chunk_nib[128];      // 4-bit windows of x^(8 * 32 KiB)
+  uint32_t chunk_pw[3][256];    // x^(8 * 32 KiB * t * 256^r)
+  uint32_t byte_pw[5][256];     // x^(8 * t * 256^r)
+};
+
+constexpr CrcTables make_tables() {
+  CrcTables t{};
+  uint32_t p = 1u << 30;  // x^1
+  for (int i = 0; i < 64; ++i) {
+    t.x2k[i] = p;
+    p = gf2_mul(p, p);
+  }
+  const uint32_t y = t.x2k[12];  // x^4096
+  for (int k = 0; k < 4; ++k)
+    for (int e = 0; e < 256; ++e) t.ybase[k][e] = gf2_mul(y, (uint32_t)e << (8 * k));
+  uint32_t lconst[32] = {};
+  for (int l = 0; l < 32; ++l) lconst[l] = xpow_bits(t.x2k, 128ull * (31 - l));
+  for (int idx = 0; idx < 8 * 16 * 32; ++idx) {
+    const int l = idx & 31, pv = idx >> 5, pp = pv >> 4, v = pv & 15;
+    t.lanetab[idx] = gf2_mul(lconst[l], (uint32_t)v << (4 * pp));
+  }
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t m = xpow_bits(t.x2k, 32ull * (4 - c));
+    for (int w = 0; w < 128; ++w) t.nib4[c][w] = gf2_mul(m, (uint32_t)(w & 15) << (4 * (w >> 4)));
+  }
+  for (int e = 0; e < 256; ++e) {
+    uint32_t c = (uint32_t)e;
+    for (int b = 0; b < 8; ++b) c = (c & 1u) ? (c >> 1) ^ kPoly : c >> 1;
+    t.t8[e] = c;
+  }
+  const uint32_t chunk = xpow_bits(t.x2k, (uint64_t)kChunk * 8);
+  for (int w = 0; w < 128; ++w) t.chunk_nib[w] = gf2_mul(chunk, (uint32_t)(w & 15) << (4 * (w >> 4)));
+  for (int r = 0; r < 3; ++r) {
+    const uint32_t base = xpow_bits(t.x2k, ((uint64_t)kChunk * 8) << (8 * r));
+    uint32_t acc = 1u << 31;
+    for (int e = 0; e < 256; ++e, acc = gf2_mul(acc, base)) t.chunk_pw[r][e] = acc;
+  }
+  for (int r = 0; r < 5; ++r) {
+    const uint32_t base = xpow_bits(t.x2k, 8ull << (8 * r));
+    uint32_t acc = 1u << 31;
+    for (int e = 0; e < 256; ++e, acc = gf2_mul(acc, base)) t.byte_pw[r][e] = acc;
+  }
+  return t;
+}
+
+__device__ const CrcTables kTab = make_tables();
+
+// x^(8 n) mod P: five byte-power lookups for n < 2^40, the x^(2^k) walk above
+__device__ __forceinline__ uint32_t xpow_bytes(uint64_t n) {
+  if (n >> 40) return xpow_bits(kTab.x2k, n << 3);
+  uint32_t acc = __ldg(&kTab.byte_pw[0][n & 255]);
+  for (int r = 1; r < 5 && (n >> (8 * r)); ++r)
+    acc = gf2_mul(acc, __ldg(&kTab.byte_pw[r][(n >> (8 * r)) & 255]));
+  return acc;
+}
+
+__device__ __forceinline__ uint32_t shift_bytes(uint32_t r, uint64_t n) {
+  return n ? gf2_mul(xpow_bytes(n), r) : r;
 }
 
 __device__ __forceinline__ uint32_t mul_const(const uint32_t* nib, uint32_t b) {
@@ -207,8 +264,7 @@ __device__ __forceinline__ ChunkRef chunk_ref(const pec_copy_desc* __restrict__ 
 template <bool kStore>
 __global__ void __launch_bounds__(kThreads, 1)
 pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
-                const uint64_t* __restrict__ total_dev, CrcConsts k,
-                uint32_t* __restrict__ chunk_raw) {
+                const uint64_t* __restrict__ total_dev, uint32_t* __restrict__ chunk_raw) {
   const uint64_t total_cap = total;       // scratch is sized for the launch bound
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* ytab = reinterpret_cast<uint32_t*>(smem);
@@ -219,45 +275,26 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
   uint8_t* ring = reinterpret_cast<uint8_t*>(x2k + 64);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)kWarps * kRing * kStage);
   __shared__ QueueEntry queue[kWarps * kQueue];
-  __shared__ uint32_t lconst[32];
-  __shared__ uint32_t base[4][256];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   if (total_dev != nullptr) {
     const uint64_t td = *total_dev;
     total = td < total ? td : total;
   }
-  // ---- tables ----------------------------------------------------------------
-  if (tid < 64) x2k[tid] = k.x2k[tid];
+  // ---- tables: copied from the compile-time constants ------------------------
   if (tid == 0) {
     for (int s = 0; s < kWarps * kRing; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int idx = tid; idx < 1024; idx += kThreads) {
-    const int tk = idx >> 8, e = idx & 255;
-    base[tk][e] = gf2_mul(k.y, (uint32_t)e << (8 * tk));
-  }
-  {
-    uint32_t c = (uint32_t)tid;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) c = (c & 1u) ? (c >> 1) ^ kPoly : c >> 1;
-    t8[tid] = c;
-  }
-  __syncthreads();
-  if (tid < 32) lconst[tid] = xpow_bits(x2k, 128ull * (31 - tid));
+  if (tid < 64) x2k[tid] = kTab.x2k[tid];
+  t8[tid] = kTab.t8[tid];
   for (int idx = tid; idx < kYtabWords; idx += kThreads) {
     // word 64 e + 32 b + 16 o + g holds table k = b | (o << 1), entry e
-    ytab[idx] = base[((idx >> 5) & 1) | (((idx >> 4) & 1) << 1)][idx >> 6];
+    ytab[idx] = __ldg(&kTab.ybase[((idx >> 5) & 1) | (((idx >> 4) & 1) << 1)][idx >> 6]);
   }
-  for (int idx = tid; idx < kNibWords; idx += kThreads) {
-    const int t = idx >> 7, p = (idx >> 4) & 7, v = idx & 15;
-    nib[idx] = gf2_mul(xpow_bits(x2k, 32ull * (4 - t)), (uint32_t)v << (4 * p));
-  }
-  __syncthreads();
-  for (int idx = tid; idx < kLaneTabWords; idx += kThreads) {
-    const int l = idx & 31, pv = idx >> 5, p = pv >> 4, v = pv & 15;
-    lanetab[idx] = gf2_mul(lconst[l], (uint32_t)v << (4 * p));
-  }
+  for (int idx = tid; idx < kNibWords; idx += kThreads) nib[idx] = __ldg(&kTab.nib4[0][0] + idx);
+  for (int idx = tid; idx < kLaneTabWords; idx += kThreads)
+    lanetab[idx] = __ldg(&kTab.lanetab[idx]);
   __syncthreads();
 
   // ---- per-lane lookup geometry ----------------------------------------------
@@ -397,7 +434,7 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
         const uint32_t oc = __shfl_down_sync(0xffffffffu, c, 1 << j);
         const uint32_t ol = __shfl_down_sync(0xffffffffu, my_len, 1 << j);
         if ((lane & ((2 << j) - 1)) == 0) {
-          c = shift_bytes(x2k, c, ol) ^ oc;
+          c = shift_bytes(c, ol) ^ oc;
           my_len += ol;
         }
       }
@@ -412,8 +449,7 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
 
 template <bool kStore>
 int launch_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
-                    const uint64_t* total_chunks_dev, const CrcConsts& consts,
-                    uint32_t* chunk_crc, cudaStream_t st) {
+                    const uint64_t* total_chunks_dev, uint32_t* chunk_crc, cudaStream_t st) {
   static int ready[64] = {0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return PEC_E_CUDA;
@@ -431,7 +467,7 @@ int launch_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
   const uint64_t need = (total_chunks + kWarps - 1) / kWarps;
   if (grid > need) grid = need;
   pack_crc_kernel<kStore><<<(unsigned)grid, kThreads, kSmemBytes, st>>>(
-      descs, n, total_chunks, total_chunks_dev, consts, chunk_crc);
+      descs, n, total_chunks, total_chunks_dev, chunk_crc);
   return PEC_OK;
 }
 
@@ -446,36 +482,15 @@ int launch_pack_crc(const pec_copy_desc* descs, int n, uint64_t total_chunks,
 // the last chunk's length once per entry and joins it.
 __global__ void __launch_bounds__(256)
 crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
-                const uint64_t* __restrict__ total_dev, CrcConsts k,
+                const uint64_t* __restrict__ total_dev,
                 const uint32_t* __restrict__ chunk_raw, uint32_t* __restrict__ entry_raw) {
-  __shared__ uint32_t x2k[64];
   __shared__ uint32_t cnib[128];        // windows of x^(8 * 32768)
   __shared__ uint32_t pw[3][256];       // x^(8 * 32K * t * 256^r)
   const int tid = threadIdx.x;
-  if (tid < 64) x2k[tid] = k.x2k[tid];
+  if (tid < 128) cnib[tid] = __ldg(&kTab.chunk_nib[tid]);
+  for (int idx = tid; idx < 3 * 256; idx += blockDim.x) pw[idx >> 8][idx & 255] =
+      __ldg(&kTab.chunk_pw[0][0] + idx);
   __syncthreads();
-  if (tid < 3) {
-    const int r = tid;
-    uint32_t b = xpow_bits(x2k, ((uint64_t)kChunk * 8) << (8 * r));
-    pw[r][0] = 1u << 31;
-    for (int l = 0; l < 8; ++l) {  // pw[r][2^l] = base^(2^l)
-      pw[r][1 << l] = b;
-      b = gf2_mul(b, b);
-    }
-  }
-  __syncthreads();
-  if (tid < 128) {
-    const int p = (tid >> 4) & 7, v = tid & 15;
-    cnib[tid] = gf2_mul(pw[0][1], (uint32_t)v << (4 * p));
-  }
-  for (int l = 1; l < 8; ++l) {     // pw[t] = pw[t - 2^l] * pw[2^l] for 2^l < t < 2^(l+1)
-    const int span = (1 << l) - 1;
-    for (int idx = tid; idx < 3 * span; idx += blockDim.x) {
-      const int r = idx / span, t = (1 << l) + 1 + idx % span;
-      pw[r][t] = gf2_mul(pw[r][t - (1 << l)], pw[r][1 << l]);
-    }
-    __syncthreads();
-  }
   if (total_dev != nullptr) {
     const uint64_t td = *total_dev;
     total = td < total ? td : total;
@@ -522,7 +537,7 @@ crc_fold_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
 
 // Per entry: R = A * x^(8 * len(last chunk)) ^ R(last chunk), then the
 // initial value / final inversion: crc = ~(R ^ ~0 * x^(8 * nbytes)).
-__global__ void crc_final_kernel(const pec_copy_desc* __restrict__ d, int n, CrcConsts k,
+__global__ void crc_final_kernel(const pec_copy_desc* __restrict__ d, int n,
                                  const uint32_t* __restrict__ chunk_raw,
                                  uint32_t* __restrict__ entry) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -535,21 +550,11 @@ __global__ void crc_final_kernel(const pec_copy_desc* __restrict__ d, int n, Crc
     const uint64_t last_len = nb - ((chunks - 1) << kCrcLg);
     PEC_DCHECK(last_len > 0 && last_len <= (uint64_t)kChunk);
     const uint32_t r_last = chunk_raw[d[i].first_chunk + chunks - 1];
-    const uint32_t r = shift_bytes(k.x2k, entry[i], last_len) ^ r_last;
-    entry[i] = ~(r ^ shift_bytes(k.x2k, 0xFFFFFFFFu, nb));
+    const uint32_t r = shift_bytes(entry[i], last_len) ^ r_last;
+    entry[i] = ~(r ^ shift_bytes(0xFFFFFFFFu, nb));
   }
 }
 
-CrcConsts make_consts() {
-  CrcConsts k;
-  uint32_t p = 1u << 30;  // x^1
-  for (int i = 0; i < 64; ++i) {
-    k.x2k[i] = p;
-    p = gf2_mul(p, p);
-  }
-  k.y = k.x2k[12];        // x^4096
-  return k;
-}
 
 template <bool kStore>
 int crc_entries(const pec_copy_desc* descs, int n, uint64_t total_chunks,
@@ -559,20 +564,19 @@ int crc_entries(const pec_copy_desc* descs, int n, uint64_t total_chunks,
   if (n == 0) return PEC_OK;
   if (descs == nullptr || entry_crc == nullptr || (total_chunks > 0 && chunk_crc == nullptr))
     return PEC_E_INVAL;
-  static const CrcConsts consts = make_consts();
   cudaStream_t st = as_stream(stream);
   if (cudaMemsetAsync(entry_crc, 0, sizeof(uint32_t) * (size_t)n, st) != cudaSuccess)
     return PEC_E_CUDA;
   if (total_chunks > 0) {
-    const int rc = launch_pack_crc<kStore>(descs, n, total_chunks, total_chunks_dev, consts,
-                                           chunk_crc, st);
+    const int rc = launch_pack_crc<kStore>(descs, n, total_chunks, total_chunks_dev, chunk_crc,
+                                           st);
     if (rc != PEC_OK) return rc;
     uint64_t fold_grid = (total_chunks + 255) / 256;
     if (fold_grid > (uint64_t)sm_count()) fold_grid = (uint64_t)sm_count();  // tables per CTA
     crc_fold_kernel<<<(unsigned)fold_grid, 256, 0, st>>>(descs, n, total_chunks, total_chunks_dev,
-                                                          consts, chunk_crc, entry_crc);
+                                                          chunk_crc, entry_crc);
   }
-  crc_final_kernel<<<(n + 255) / 256, 256, 0, st>>>(descs, n, consts, chunk_crc, entry_crc);
+  crc_final_kernel<<<(n + 63) / 64, 64, 0, st>>>(descs, n, chunk_crc, entry_crc);
   return launch_status();
 }
 
