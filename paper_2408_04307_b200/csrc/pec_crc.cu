@@ -85,7 +85,18 @@ __host__ __device__ constexpr uint32_t xpow_bits(const uint32_t* x2k, uint64_t n
 // and stored in the device image: the kernels copy what they need into
 // shared memory instead of deriving it with thousands of GF(2) products per
 // launch (round-1/early round-2 kernels built them per CTA).
-struct CrcTables {
+// The pack kernel's shared-memory tables, laid out exactly as the kernel
+// uses them, so one TMA bulk copy fills them per CTA.
+struct alignas(16) SmemImage {
+  uint32_t ytab[256 * 64];      // entry e, table k, lane group g at word 64 e + 32 (k & 1) + 16 (k >> 1) + g
+  uint32_t lanetab[8 * 16 * 32];  // lane l's 4-bit windows of x^(128 (31 - l)), [p][v][l]
+  uint32_t nib4[4 * 128];       // 4-bit windows of x^(32 (4 - t)), t = 0..3
+  uint32_t t8[256];             // the standard byte table (partial chunks)
+  uint32_t x2k[64];             // x^(2^k) mod P
+};
+
+struct alignas(16) CrcTables {
+  SmemImage img;
   uint32_t x2k[64];             // x^(2^k) mod P
   uint32_t ybase[4][256];       // slicing-by-4 tables of Y = x^4096: T_k[e] = Y * (e << 8k)
   uint32_t lanetab[8 * 16 * 32];  // lane l's 4-bit windows of x^(128 (31 - l)), [p][v][l]
@@ -121,6 +132,12 @@ constexpr CrcTables make_tables() {
     for (int b = 0; b < 8; ++b) c = (c & 1u) ? (c >> 1) ^ kPoly : c >> 1;
     t.t8[e] = c;
   }
+  for (int idx = 0; idx < 256 * 64; ++idx)   // 16x replicated, tables 0/1 and 2/3 in bank halves
+    t.img.ytab[idx] = t.ybase[((idx >> 5) & 1) | (((idx >> 4) & 1) << 1)][idx >> 6];
+  for (int idx = 0; idx < 8 * 16 * 32; ++idx) t.img.lanetab[idx] = t.lanetab[idx];
+  for (int idx = 0; idx < 4 * 128; ++idx) t.img.nib4[idx] = t.nib4[idx >> 7][idx & 127];
+  for (int e = 0; e < 256; ++e) t.img.t8[e] = t.t8[e];
+  for (int i = 0; i < 64; ++i) t.img.x2k[i] = t.x2k[i];
   const uint32_t chunk = xpow_bits(t.x2k, (uint64_t)kChunk * 8);
   for (int w = 0; w < 128; ++w) t.chunk_nib[w] = gf2_mul(chunk, (uint32_t)(w & 15) << (4 * (w >> 4)));
   for (int r = 0; r < 3; ++r) {
@@ -185,6 +202,12 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
       "[%0], [%1], %2, [%3], %4;"
       :: "r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_plain(void* smem, const void* gmem, uint32_t bytes,
+                                               uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      :: "r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes,
                                          uint64_t policy) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
@@ -212,7 +235,10 @@ __device__ __forceinline__ void bulk_wait_all() {
 constexpr int kYtabWords = 256 * 64;
 constexpr int kLaneTabWords = 8 * 16 * 32;
 constexpr int kNibWords = 4 * 128;
-constexpr size_t kSmemBytes = (size_t)(kYtabWords + kLaneTabWords + kNibWords + 256 + 64) * 4 +
+static_assert(sizeof(SmemImage) == (size_t)(kYtabWords + kLaneTabWords + kNibWords + 256 + 64) * 4,
+              "shared-memory table image layout");
+static_assert(sizeof(SmemImage) % 16 == 0, "TMA bulk copies move multiples of 16 bytes");
+constexpr size_t kSmemBytes = sizeof(SmemImage) +
                               (size_t)kWarps * kRing * kStage + (size_t)kWarps * kRing * 8;
 
 // One chain step S * Y ^ w: four table lookups at PRMT-formed byte offsets
@@ -281,21 +307,19 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
     const uint64_t td = *total_dev;
     total = td < total ? td : total;
   }
-  // ---- tables: copied from the compile-time constants ------------------------
+  // ---- tables: one TMA bulk copy of the compile-time image ---------------------
+  __shared__ __align__(8) uint64_t table_bar;
   if (tid == 0) {
     for (int s = 0; s < kWarps * kRing; ++s) mbar_init(&bars[s], 1);
+    mbar_init(&table_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < 64) x2k[tid] = kTab.x2k[tid];
-  t8[tid] = kTab.t8[tid];
-  for (int idx = tid; idx < kYtabWords; idx += kThreads) {
-    // word 64 e + 32 b + 16 o + g holds table k = b | (o << 1), entry e
-    ytab[idx] = __ldg(&kTab.ybase[((idx >> 5) & 1) | (((idx >> 4) & 1) << 1)][idx >> 6]);
-  }
-  for (int idx = tid; idx < kNibWords; idx += kThreads) nib[idx] = __ldg(&kTab.nib4[0][0] + idx);
-  for (int idx = tid; idx < kLaneTabWords; idx += kThreads)
-    lanetab[idx] = __ldg(&kTab.lanetab[idx]);
   __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(&table_bar, (uint32_t)sizeof(SmemImage));
+    bulk_g2s_plain(smem, &kTab.img, (uint32_t)sizeof(SmemImage), &table_bar);
+  }
+  mbar_wait(&table_bar, 0);
 
   // ---- per-lane lookup geometry ----------------------------------------------
   // step s: the lower half-warp reads byte s of S from table s, the upper
