@@ -254,7 +254,7 @@ __device__ __forceinline__ uint32_t ystep(const uint8_t* ytab, uint32_t S, uint3
   return a[0] ^ a[1] ^ a[2] ^ a[3] ^ w;
 }
 
-constexpr int kQueue = 4;                       // claimed chunks queued per warp
+constexpr int kQueue = 2;   // claimed chunks queued per warp (few: claims held ahead unbalance the tail)
 
 struct QueueEntry {
   const uint8_t* src;
