@@ -1,7 +1,8 @@
 """Versioned, CRC-32C-checked, completion-marked checkpoint store.
 
-Host mirror of `pkg/src/mocsim/store.py` with the same on-disk format, byte
-for byte (store.py:1-8, 149-228):
+The on-disk format is the reference's (`pkg/src/mocsim/store.py`), byte for
+byte (store.py:1-8, 149-228), so either implementation reads the other's
+versions:
 
     v%06d/rank%04d/<store_key>.bin   entry payloads
     v%06d/meta.json                  json.dumps(sort_keys=True, indent=0) + "\\n"
@@ -11,8 +12,9 @@ for byte (store.py:1-8, 149-228):
 What changes on B200 is the payload: the reference writes a synthetic
 blake2b stand-in per entry (store.py:118-121); here `write_version` takes
 the real snapshot bytes (``payloads``: store_key -> bytes-like, normally
-views into a pinned host snapshot buffer), CRCs them with the multithreaded
-SSE4.2 CRC-32C of libpec, and writes the entry files from a thread pool.
+views into a pinned host snapshot buffer) with their CRC-32Cs computed by the
+pack on the GPU (``crcs``; libpec's multithreaded SSE4.2 CRC-32C otherwise)
+and writes the entry files with the native writer (`pec_write_files`).
 Without ``payloads`` it falls back to the reference's synthetic payloads,
 so metadata-only callers (the reference's own engine tests) behave exactly as
 before.  Manifest ``size`` is the payload length in both cases.
