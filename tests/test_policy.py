@@ -59,3 +59,29 @@ def test_measured_bandwidths_feed_the_configurator():
     ref = adaptive_configure_layout(layout, "adaptive_pec", base)
     assert ref.pec.k_snapshot < cfg.pec.k_snapshot
     assert cfg.i_ckpt >= 1
+
+
+def test_b200_cadence_floors_follow_the_measured_rates():
+    """policy.b200_cadence (the cadence bench.py's stall leg runs at): each
+    floor is ceil(bottleneck time / iteration) for its tier, the minimum
+    interval is their maximum, and a slower persist tier never lowers it."""
+    import math
+    from dataclasses import replace
+    from paper_2408_04307_b200 import bottleneck_workload, plan_adaptive
+    from paper_2408_04307_b200.policy import b200_cadence
+    w = configs.mixtral_8x7b()
+    layout = w.layout()
+    worst = max(bottleneck_workload(plan_adaptive(layout, w.pec), p)[1] for p in range(8))
+    base = replace(layout.cluster, snapshot_bandwidth=3.3e12, fb_time=0.1, update_time=0.025)
+    prev = 0
+    for persist_gbs in (40, 15, 8, 4):
+        cl = replace(base, persist_bandwidth=persist_gbs * 1e9)
+        cad = b200_cadence(layout, w.strategy, w.pec, cl, drain_bw=56e9)
+        iter_s = 0.125
+        assert cad.persist_floor == max(1, math.ceil(worst / (persist_gbs * 1e9) / iter_s - 1e-9))
+        assert cad.drain_floor == max(1, math.ceil(worst / 56e9 / iter_s - 1e-9))
+        assert cad.snapshot_floor == 1          # a 3.8 ms pack hides under a 100 ms F&B
+        assert cad.i_ckpt_min == max(cad.persist_floor, cad.drain_floor, cad.snapshot_floor)
+        assert cad.i_ckpt_min >= prev
+        prev = cad.i_ckpt_min
+    assert prev > 10                            # 4 GB/s persist: I_ckpt = 10 is infeasible

@@ -114,3 +114,41 @@ def test_split_table_covers_each_copy_exactly_once(seed):
             k += 1
         assert off == n
     assert k == len(pieces)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_spans_cover_agrees_with_a_byte_mask(seed):
+    """engine.spans_cover (the memory-source coverage of resolve_recovery,
+    reference engine.py:257-258) == painting the spans into a byte mask."""
+    import random
+    from paper_2408_04307_b200.engine import spans_cover
+    rng = random.Random(seed)
+    size = rng.randint(1, 64)
+    for _ in range(50):
+        spans = [(lo, lo + rng.randint(0, 20)) for lo in
+                 (rng.randint(0, size) for _ in range(rng.randint(1, 6)))]
+        mask = [False] * size
+        for lo, hi in spans:
+            for b in range(lo, min(hi, size)):
+                mask[b] = True
+        # the reference's rule: sorted by start, no gap before `size`
+        reach, ok = 0, True
+        for lo, hi in sorted(spans):
+            if lo > reach:
+                ok = False
+                break
+            reach = max(reach, hi)
+        assert spans_cover(spans, size) == (ok and reach >= size)
+        if spans_cover(spans, size):
+            assert all(mask)
+
+
+@pytest.mark.parametrize("n", [1, 3, 8, 16])
+def test_window_table_rows_are_the_per_layer_windows(n):
+    from paper_2408_04307_b200.selector import select_window, window_table
+    for width in range(1, n + 2):
+        for stride in range(0, n + 1):
+            for c in range(0, 2 * n + 1):
+                tab = window_table(c, 5, n, width, stride)
+                for m in range(5):
+                    assert tab[m].tolist() == sorted(select_window(c, m, n, width, stride))
