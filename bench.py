@@ -455,25 +455,48 @@ def build_workload(args, rank):
     return w, layout, plan
 
 
-def prune_store(store, keep: int = 1) -> None:
-    """Bench-only retention: drop all but the newest ``keep`` complete
-    versions (each is a full rank shard; /dev/shm is host RAM)."""
+def prune_store(store, keep: int = 1, ranks=None, coordinator: bool = True) -> int:
+    """Bench-only retention of a /dev/shm persist tier (host RAM): of every
+    complete version but the newest ``keep``, delete the rank directories of
+    ``ranks`` (each rank process deletes its own: freeing tmpfs pages runs at
+    ~10-20 GB/s per thread, so one deleter cannot keep up with N ranks'
+    versions), and — on the coordinator — the version directory itself once
+    no rank directory is left.  Returns the number of old versions still
+    present."""
     if store is None or not hasattr(store, "version_dir"):
-        return
+        return 0
     import shutil
-    for v in store.complete_versions()[:-keep]:
-        shutil.rmtree(store.version_dir(v), ignore_errors=True)
+    old = store.complete_versions()[:-keep] if keep else store.complete_versions()
+    left = 0
+    for v in old:
+        vdir = store.version_dir(v)
+        if ranks is None:
+            shutil.rmtree(vdir, ignore_errors=True)
+            continue
+        for r in ranks:
+            shutil.rmtree(vdir / f"rank{r:04d}", ignore_errors=True)
+        if coordinator and not any(vdir.glob("rank*")):
+            shutil.rmtree(vdir, ignore_errors=True)
+        else:
+            left += 1
+    return left
 
 
 class Retention:
-    """`prune_store` on a background thread: freeing a 12.6 GB version's
-    tmpfs pages takes ~0.5 s, which must not block the training thread (a
-    blocked launch thread starves the GPU)."""
+    """`prune_store` on a background thread of every rank: freeing a
+    version's tmpfs pages takes ~0.5 s per 12.6 GB, which must not block the
+    training thread (a blocked launch thread starves the GPU).  Memory is
+    bounded all the same: when more than ``max_old`` superseded versions are
+    still present, `submit` waits for the deleter (never observed at the
+    policy's cadence; a guard against running the node out of RAM)."""
 
-    def __init__(self, store, keep: int = 1):
+    def __init__(self, store, ranks, coordinator: bool, keep: int = 1, max_old: int = 1):
         import queue
-        self.store, self.keep = store, keep
+        self.store, self.keep, self.ranks = store, keep, list(ranks)
+        self.coordinator, self.max_old = coordinator, max_old
         self.q = queue.Queue()
+        self.left = 0
+        self.waited_s = 0.0
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
 
@@ -481,17 +504,33 @@ class Retention:
         while True:
             item = self.q.get()
             if item is None:
+                self.q.task_done()
                 return
-            prune_store(self.store, self.keep)
+            self.left = prune_store(self.store, self.keep, self.ranks, self.coordinator)
             self.q.task_done()
 
     def submit(self):
+        if len(self.store.complete_versions()) - self.keep > self.max_old:
+            t0 = time.perf_counter()
+            self.q.join()                       # back-pressure: let the deleter catch up
+            self.waited_s += time.perf_counter() - t0
         if self.q.empty():
             self.q.put(1)
 
     def close(self):
         self.q.put(None)
         self.t.join()
+
+
+def sweep_stale_stores(base: str = "/dev/shm") -> None:
+    """Remove persist stores of earlier bench runs whose process is gone (a
+    killed run leaves its versions in host RAM)."""
+    import glob
+    import shutil
+    for d in glob.glob(os.path.join(base, "pec_bench_*")):
+        owner = os.path.basename(d).split("_")[2] if d.count("_") >= 3 else ""
+        if owner.isdigit() and not os.path.exists(f"/proc/{owner}"):
+            shutil.rmtree(d, ignore_errors=True)
 
 
 def measure_host_link(eng, world, dev):
@@ -566,7 +605,8 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
     iters = (n_ckpt + 1) * i_ckpt
     store = ck.engine.store
     stats = ck.engine.stats
-    retention = Retention(store) if (rank == 0 and store is not None) else None
+    retention = Retention(store, ranks=[rank], coordinator=rank == 0) \
+        if store is not None else None
 
     def run(with_ckpt: bool, base_it: int):
         barrier(world)
@@ -618,8 +658,10 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
         waits_all.append(waits)
         persists += pers
         hosts.append({k: (round(v, 3) if isinstance(v, float) else v) for k, v in host.items()})
+    retention_wait_s = 0.0
     if retention is not None:
         retention.close()
+        retention_wait_s = retention.waited_s
     without = max_over_ranks(statistics.mean(runs_without), world, dev)
     with_ = max_over_ranks(statistics.mean(runs_with), world, dev)
     packs = stats["pack_ms"][-rounds * n_ckpt:]
@@ -649,6 +691,7 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
                                   "GBps": round(shard / statistics.mean(persists) / 1e9, 2)
                                   if persists else None},
             "window": "every drain and persist of the arm completes inside the timed window",
+            "retention_backpressure_s": round(retention_wait_s, 3),
             "diag_with_arms": hosts}
 
 
@@ -683,7 +726,10 @@ def run_b200(args):
     if persist != "none":
         # one store root for all ranks (multi-writer commit, distributed.py)
         base = "/dev/shm" if persist == "shm" else tempfile.gettempdir()
-        root = [tempfile.mkdtemp(prefix="pec_bench_", dir=base) if rank == 0 else None]
+        if rank == 0:
+            sweep_stale_stores(base)
+        root = [tempfile.mkdtemp(prefix=f"pec_bench_{os.getpid()}_", dir=base)
+                if rank == 0 else None]
         if world > 1:
             import torch.distributed as dist
             dist.broadcast_object_list(root, src=0)
@@ -890,8 +936,7 @@ def run_b200(args):
                             "crc": "device (pack)" if mode == D.MODE_CRC else "host",
                             "seconds": round(p_s, 3),
                             "GBps": round(eng.stats["snap_bytes"][-1] / p_s / 1e9, 2)}
-            if rank == 0:
-                prune_store(store)
+            prune_store(store, ranks=[rank], coordinator=rank == 0)
 
         # ---- the cadence the policy derives from this run's measurements ------
         if store is not None and not args.no_stall:
