@@ -479,7 +479,7 @@ def test_gpt350m_k_sweep_pack_bit_exact_on_device(dev, k):
     full size) and the staged payload equals the reference planner's
     per-rank workload."""
     import torch
-    from paper_2408_04307_b200 import configs, plan_adaptive, plan_equal
+    from paper_2408_04307_b200 import configs, plan_adaptive
     from paper_2408_04307_b200.arena import StateArena
     from paper_2408_04307_b200 import device as D
     from paper_2408_04307_b200.staging import DeviceTable, StagingLayout
