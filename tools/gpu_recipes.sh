@@ -68,7 +68,7 @@ case "$recipe" in
     timeout 600 python tools/guard_kernels.py > $O/guard_release.txt 2>&1; echo guard_release=$?
     PEC_LIB=debug timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider \
       > $O/gpu_suite_debug_lib.txt 2>&1; echo suite_debug=$?
-    tail -2 $O/guard_debug.txt $O/guard_release.txt $O/gpu_suite_debug_lib.txt
+    tail -n 2 $O/guard_debug.txt $O/guard_release.txt $O/gpu_suite_debug_lib.txt
     ;;
   host_link)   # pinned D2H / push probes
     timeout 300 python tools/d2h_probe.py > $O/d2h_probe.json 2>&1; cat $O/d2h_probe.json
