@@ -456,30 +456,34 @@ def build_workload(args, rank):
 
 
 def prune_store(store, keep: int = 1, ranks=None, coordinator: bool = True) -> int:
-    """Bench-only retention of a /dev/shm persist tier (host RAM): of every
-    complete version but the newest ``keep``, delete the rank directories of
-    ``ranks`` (each rank process deletes its own: freeing tmpfs pages runs at
-    ~10-20 GB/s per thread, so one deleter cannot keep up with N ranks'
-    versions), and — on the coordinator — the version directory itself once
-    no rank directory is left.  Returns the number of old versions still
-    present."""
+    """Bench-only retention of a /dev/shm persist tier (host RAM): every
+    version older than the newest ``keep`` complete ones is retired — each
+    rank process retires its own rank directories (freeing or recycling
+    tmpfs pages runs at ~10-20 GB/s per thread, so one deleter cannot keep
+    up with N ranks' versions) and the coordinator removes the version
+    itself once no rank directory is left (`DiskStore.retire`; with
+    ``recycle`` the entry files become spares later versions overwrite in
+    place).  Returns the number of old versions still present."""
     if store is None or not hasattr(store, "version_dir"):
         return 0
-    import shutil
-    old = store.complete_versions()[:-keep] if keep else store.complete_versions()
+    complete = store.complete_versions()
+    if len(complete) <= keep:
+        return 0
+    cutoff = complete[-keep] if keep else complete[-1] + 1
     left = 0
-    for v in old:
-        vdir = store.version_dir(v)
-        if ranks is None:
-            shutil.rmtree(vdir, ignore_errors=True)
-            continue
-        for r in ranks:
-            shutil.rmtree(vdir / f"rank{r:04d}", ignore_errors=True)
-        if coordinator and not any(vdir.glob("rank*")):
-            shutil.rmtree(vdir, ignore_errors=True)
-        else:
+    for v in store.version_numbers():
+        if v >= cutoff:
+            break
+        if not store.retire(v, ranks=ranks, coordinator=coordinator):
             left += 1
+    if ranks is not None and getattr(store, "recycle", False):
+        # spares beyond one version's worth of this rank's files are dropped
+        store.trim_spares(ranks, keep_bytes=store_bytes_per_version.get(id(store), 1 << 62))
     return left
+
+
+# bench-side record of one version's bytes per rank (the spare-pool cap)
+store_bytes_per_version = {}
 
 
 class Retention:
@@ -510,7 +514,7 @@ class Retention:
             self.q.task_done()
 
     def submit(self):
-        if len(self.store.complete_versions()) - self.keep > self.max_old:
+        if len(self.store.version_numbers()) - self.keep - 1 > self.max_old:
             t0 = time.perf_counter()
             self.q.join()                       # back-pressure: let the deleter catch up
             self.waited_s += time.perf_counter() - t0
@@ -735,7 +739,8 @@ def run_b200(args):
             dist.broadcast_object_list(root, src=0)
         store_root = root[0]
         store = DiskStore(store_root, io_threads=args.persist_threads or
-                          len(os.sched_getaffinity(0)), direct_io=args.direct_io)
+                          len(os.sched_getaffinity(0)), direct_io=args.direct_io,
+                          recycle=persist == "shm" and not args.no_recycle)
     mode = {"vec": D.MODE_VEC, "bulk": D.MODE_BULK, "crc": D.MODE_CRC}[args.engine]
     # the persist protocol gets its own gloo group (created collectively inside)
     ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=1, ranks=[rank],
@@ -743,6 +748,8 @@ def run_b200(args):
     eng = ck.engine
     eng.pipelined_drain = not args.no_pipelined_drain
     eng.reserve(ck.max_snapshot_bytes(), host_buffers=0)
+    if store is not None:
+        store_bytes_per_version[id(store)] = ck.max_snapshot_bytes() + (64 << 20)
     k_s = w.pec.k_snapshot
     sel = torch.empty((L, min(k_s, E)), dtype=torch.int32, device=dev)
     stream = eng.pack_stream
@@ -1093,6 +1100,9 @@ def main():
                     help="persist with O_DIRECT (meaningful with --persist disk)")
     ap.add_argument("--persist-threads", type=int, default=0,
                     help="writer threads per rank (0 = all host cores; background priority)")
+    ap.add_argument("--no-recycle", action="store_true",
+                    help="retire superseded /dev/shm versions by deleting their files instead "
+                         "of recycling them as spares (A/B)")
     ap.add_argument("--stall-no-persist", action="store_true",
                     help="diagnostic: run the stall leg with the persist tier off")
     ap.add_argument("--no-e2e", action="store_true")

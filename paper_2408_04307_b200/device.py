@@ -355,12 +355,14 @@ def crc32c_many(base, offsets, lengths, threads: Optional[int] = None) -> np.nda
 
 
 def write_files(paths, buffers, threads: Optional[int] = None, want_crc: bool = True,
-                fsync: bool = False, direct: bool = False, background: bool = False):
+                fsync: bool = False, direct: bool = False, background: bool = False,
+                overwrite: bool = False):
     """Native multi-threaded writer (pec_write_files): file i <- buffers[i]
     (bytes-like / ndarray / CPU tensor).  Returns the CRC-32C of each file
     (uint32 ndarray) when ``want_crc``.  ``direct`` opens files O_DIRECT
     (page-cache bypass; buffered where the filesystem refuses it; large files
-    range-parallel); ``background`` runs the writer threads at nice +10."""
+    range-parallel); ``background`` runs the writer threads at nice +10;
+    ``overwrite`` rewrites existing files in place (recycled files)."""
     n = len(paths)
     keep = [_host_buffer(b) for b in buffers]
     c_paths = (ctypes.c_char_p * n)(*[os.fsencode(str(p)) for p in paths])
@@ -374,7 +376,7 @@ def write_files(paths, buffers, threads: Optional[int] = None, want_crc: bool = 
                                lens.ctypes.data if n else None, n,
                                out.ctypes.data if want_crc and n else None, int(threads),
                                (1 if fsync else 0) | (2 if direct else 0) |
-                               (4 if background else 0))
+                               (4 if background else 0) | (8 if overwrite else 0))
     _check(rc, "pec_write_files")
     del keep
     return out

@@ -30,6 +30,7 @@ from __future__ import annotations
 import hashlib
 import json
 import os
+import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -194,20 +195,26 @@ class DiskStore:
     """One directory per version under ``root`` (store.py:171-282)."""
 
     def __init__(self, root, io_threads: int = 8, direct_io: bool = False, fsync: bool = False,
-                 background: bool = True):
+                 background: bool = True, recycle: bool = False):
         """B200 additions: ``io_threads`` for the native writer/reader,
         ``direct_io`` writes real payloads with O_DIRECT (page-cache bypass
         on real storage, large files range-parallel; buffered where the
         filesystem refuses it), ``fsync`` makes every entry file durable
         before the version is published, ``background`` runs the writer
         threads at nice +10 (a persist yields host cores to the training
-        loop's launch thread)."""
+        loop's launch thread), ``recycle`` lets `retire` keep a superseded
+        version's entry files as spares that later versions overwrite in
+        place (on tmpfs / page-cache targets rewriting a file keeps its
+        pages: 1.7-2.6x faster than truncating and rewriting it)."""
         self.root = Path(root)
         self.root.mkdir(parents=True, exist_ok=True)
         self.io_threads = max(1, io_threads)
         self.direct_io = direct_io
         self.fsync = fsync
         self.background = background
+        self.recycle = recycle
+        self._spares: Dict[int, Dict[int, List[Path]]] = {}   # rank -> size -> files
+        self._spare_lock = threading.Lock()
 
     def version_dir(self, version: int) -> Path:
         return self.root / f"v{version:06d}"
@@ -256,9 +263,10 @@ class DiskStore:
             # native writer: threads take whole files (largest first) and CRC
             # each 4 MiB piece right after writing it
             paths = [vdir / _entry_path(e.rank, e.store_key) for e in entries]
+            reused = self._adopt_spares(entries, data, paths) if self.recycle else 0
             got = _dev.write_files(paths, data, threads=self.io_threads, want_crc=not given,
                                    fsync=self.fsync, direct=self.direct_io,
-                                   background=self.background)
+                                   background=self.background, overwrite=reused > 0)
             crc_list = [crcs[e.store_key] for e in entries] if given else [int(c) for c in got]
             return [(e.store_key, _entry_path(e.rank, e.store_key), _nbytes(p), c)
                     for e, p, c in zip(entries, data, crc_list)]
@@ -273,6 +281,82 @@ class DiskStore:
             with ThreadPoolExecutor(max_workers=min(self.io_threads, len(entries))) as ex:
                 list(ex.map(lambda rp: self._put(vdir / rp[0][1], rp[1], None), zip(rows, data)))
         return rows
+
+    # -- recycling (B200 addition; never changes what a reader sees) -----------
+    def _spare_dir(self, rank: int) -> Path:
+        return self.root / ".spare" / f"rank{rank:04d}"
+
+    def _adopt_spares(self, entries, data, paths) -> int:
+        """Rename a spare file of exactly the payload's size onto each entry
+        path (same filesystem: O(1)); the writer then overwrites it in place.
+        Returns how many entries got one."""
+        n = 0
+        with self._spare_lock:
+            for e, p, path in zip(entries, data, paths):
+                pool = self._spares.get(e.rank, {}).get(_nbytes(p))
+                if pool:
+                    os.replace(pool.pop(), path)
+                    n += 1
+        return n
+
+    def retire(self, version: int, ranks: Optional[Iterable[int]] = None,
+               coordinator: bool = True) -> bool:
+        """Drop a superseded version (retention), keeping its entry files of
+        ``ranks`` (all ranks by default) as spares when ``recycle`` is set.
+        The COMPLETE marker goes first, so a half-retired version is never
+        readable; the coordinator removes the directory once no rank
+        directory is left.  Returns True when the version is gone."""
+        import shutil
+        import uuid
+        vdir = self.version_dir(version)
+        if not vdir.exists():
+            return True
+        if coordinator:
+            try:
+                os.unlink(vdir / "COMPLETE")
+            except FileNotFoundError:
+                pass
+        rank_dirs = sorted(vdir.glob("rank*")) if ranks is None else \
+            [vdir / f"rank{r:04d}" for r in ranks]
+        for rd in rank_dirs:
+            if not rd.exists():
+                continue
+            r = int(rd.name[4:])
+            if self.recycle:
+                spare = self._spare_dir(r)
+                spare.mkdir(parents=True, exist_ok=True)
+                for f in rd.glob("*.bin"):
+                    size = f.stat().st_size
+                    dst = spare / f"{size}.{uuid.uuid4().hex}.bin"
+                    os.replace(f, dst)
+                    with self._spare_lock:
+                        self._spares.setdefault(r, {}).setdefault(size, []).append(dst)
+            shutil.rmtree(rd, ignore_errors=True)
+        if coordinator and not any(vdir.glob("rank*")):
+            shutil.rmtree(vdir, ignore_errors=True)
+            return True
+        return False
+
+    def trim_spares(self, ranks: Iterable[int], keep_bytes: int) -> None:
+        """Delete spare files beyond ``keep_bytes`` per rank (sizes no
+        version asked for again stay bounded)."""
+        for r in ranks:
+            with self._spare_lock:
+                pool = self._spares.get(r, {})
+                files = [(size, p) for size, ps in pool.items() for p in ps]
+                total = sum(size for size, _ in files)
+                drop = []
+                for size, p in sorted(files, reverse=True):
+                    if total <= keep_bytes:
+                        break
+                    pool[size].remove(p)
+                    drop.append(p)
+                    total -= size
+            for p in drop:
+                try:
+                    os.unlink(p)
+                except FileNotFoundError:
+                    pass
 
     def publish(self, version: int, iteration: int, checkpoint_index: int,
                 entries: Iterable[StoreEntry], rows: Iterable[Tuple[str, str, int, int]],
@@ -317,6 +401,14 @@ class DiskStore:
         return self.publish(version, iteration, checkpoint_index, entries, rows, injector)
 
     # -- reading ------------------------------------------------------------
+    def version_numbers(self) -> List[int]:
+        """Every version directory present, complete or not (retention)."""
+        found = []
+        for child in self.root.iterdir():
+            if child.name.startswith("v") and child.name[1:].isdigit():
+                found.append(int(child.name[1:]))
+        return sorted(found)
+
     def complete_versions(self) -> List[int]:
         found = []
         for child in self.root.iterdir():

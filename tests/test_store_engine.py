@@ -289,3 +289,38 @@ def test_durable_store_fsyncs_and_still_reads_back(tmp_path):
         assert (tmp_path / "d" / "v000001" / f).read_bytes() == \
             (tmp_path / "p" / "v000001" / f).read_bytes()
     assert durable.manifest(1).entries["neo.r1"][2] == crc32c(pay["neo.r1"])
+
+
+@pytest.mark.parametrize("recycle", [False, True])
+def test_retire_recycles_files_without_changing_what_readers_see(tmp_path, recycle):
+    """DiskStore.retire (bench retention): a retired version disappears for
+    readers at once (COMPLETE first); with ``recycle`` its entry files become
+    spares that the next version of the same sizes overwrites in place
+    (same inodes: no page reclaim), and every version still reads back
+    CRC-verified and byte-identical to a fresh store's tree."""
+    import os
+    st = DiskStore(tmp_path / "s", io_threads=3, recycle=recycle)
+    ref = DiskStore(tmp_path / "r", io_threads=3)
+    rng = np.random.default_rng(9)
+    ents = _entries()
+    for v in (1, 2, 3):
+        pay = {e.store_key: rng.bytes(e.stop - e.start) for e in ents}
+        if v == 3:
+            inodes = {p.stat().st_ino for p in (tmp_path / "s").rglob("*.bin")
+                      if ".spare" in str(p)}
+        st.write_version(v, iteration=10 * v, checkpoint_index=v, entries=ents, payloads=pay)
+        ref.write_version(v, iteration=10 * v, checkpoint_index=v, entries=ents, payloads=pay)
+        assert st.load_checkpoint(v) == pay
+        if v == 2:
+            assert st.retire(1) is True
+            assert st.complete_versions() == [2]
+            assert not (tmp_path / "s" / "v000001").exists()
+    got = {p.stat().st_ino for p in (tmp_path / "s" / "v000003").rglob("*.bin")}
+    assert bool(got & inodes) == recycle         # v3 overwrote v1's files in place
+    for v in (2, 3):
+        for name in ("meta.json", "manifest.tsv"):
+            assert (tmp_path / "s" / f"v{v:06d}" / name).read_bytes() == \
+                (tmp_path / "r" / f"v{v:06d}" / name).read_bytes()
+    st.trim_spares([0, 1], keep_bytes=0)
+    assert not any(p.is_file() for p in (tmp_path / "s").rglob("*.bin") if ".spare" in str(p))
+    assert os.listdir(tmp_path / "s")  # the store itself remains
