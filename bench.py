@@ -467,8 +467,10 @@ def prune_store(store, keep: int = 1, ranks=None, coordinator: bool = True) -> i
     if store is None or not hasattr(store, "version_dir"):
         return 0
     complete = store.complete_versions()
-    if len(complete) <= keep:
+    if not complete or len(complete) < keep:
         return 0
+    # not `<= keep`: the coordinator unlinks COMPLETE first, so the other
+    # ranks may see only the kept versions while older ones still hold files
     cutoff = complete[-keep] if keep else complete[-1] + 1
     left = 0
     for v in store.version_numbers():
@@ -841,15 +843,16 @@ def run_b200(args):
     # host RAM next to the pinned buffers; when both do not fit, the persist
     # tier is dropped (the line says so) rather than the node running out
     shard = step_bytes
-    shm_reserve = SHM_VERSIONS_IN_FLIGHT * shard if (store is not None and persist == "shm") \
-        else 0
+    # (+1 version of spare files when retired versions are recycled)
+    shm_versions = SHM_VERSIONS_IN_FLIGHT + (1 if getattr(store, "recycle", False) else 0)
+    shm_reserve = shm_versions * shard if (store is not None and persist == "shm") else 0
     fit = host_buffers_that_fit(eng.staging.numel(), 3, reserve=shm_reserve)
     if store is not None and persist == "shm" and \
             min_over_ranks(float(fit), world, dev) < 3:
         fit_np = host_buffers_that_fit(eng.staging.numel(), 3)
         if min_over_ranks(float(fit_np), world, dev) >= 2:
             print(f"bench: host RAM ({mem_available() / 1e9:.0f} GB available) cannot hold 3 "
-                  f"pinned buffers + {SHM_VERSIONS_IN_FLIGHT} /dev/shm versions per rank; "
+                  f"pinned buffers + {shm_versions} /dev/shm versions per rank; "
                   "persist tier off", file=sys.stderr)
             persist_dropped = f"host RAM: {mem_available() / 1e9:.0f} GB available for " \
                               f"{os.environ.get('LOCAL_WORLD_SIZE', '1')} ranks"
