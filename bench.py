@@ -198,6 +198,11 @@ def host_buffers_that_fit(nbytes: int, want: int, frac: float = 0.7, reserve: in
 # one complete but not yet pruned (retention runs on a background thread)
 SHM_VERSIONS_IN_FLIGHT = 3
 
+# versions the persist probe writes before taking its rate (the policy's
+# persist bandwidth): the first ones pay tmpfs page allocation, the last one
+# is the steady-state cost
+PERSIST_PROBE_VERSIONS = 3
+
 
 def cpu_model() -> str:
     try:
@@ -936,17 +941,30 @@ def run_b200(args):
                      # the all-ranks-at-once peak is e2e.frac_of_host_link
                      "frac": round(drain_gbs / link_alone, 4)}
 
-        # ---- persist probe: one version, this run's persist rate --------------
+        # ---- persist probe: this run's steady persist rate --------------------
+        # three versions with retention between them: the first two create
+        # their files (cold tmpfs pages), the third is what every later
+        # version costs (with recycling it overwrites the first one's files)
         if store is not None:
             ck.set_persist(True)
-            ck.checkpoint(base_it + n_e2e + 1)
-            ck.finish()
-            p_s = eng.stats["persist_s"][-1]
+            probe_s = []
+            for j in range(PERSIST_PROBE_VERSIONS):
+                ck.checkpoint(base_it + n_e2e + 1 + j)
+                ck.finish()
+                probe_s.append(eng.stats["persist_s"][-1])
+                barrier(world)
+                prune_store(store, ranks=[rank], coordinator=rank == 0)
+                barrier(world)
+                prune_store(store, ranks=[rank], coordinator=rank == 0)
+            p_s = probe_s[-1]
             persist_info = {"target": persist, "direct_io": bool(args.direct_io),
                             "crc": "device (pack)" if mode == D.MODE_CRC else "host",
+                            "recycle": bool(getattr(store, "recycle", False)),
                             "seconds": round(p_s, 3),
-                            "GBps": round(eng.stats["snap_bytes"][-1] / p_s / 1e9, 2)}
-            prune_store(store, ranks=[rank], coordinator=rank == 0)
+                            "GBps": round(eng.stats["snap_bytes"][-1] / p_s / 1e9, 2),
+                            "seconds_per_probe_version": [round(x, 3) for x in probe_s],
+                            "what": f"{PERSIST_PROBE_VERSIONS} versions, retention between "
+                                    "them; seconds/GBps = the last (steady) one"}
 
         # ---- the cadence the policy derives from this run's measurements ------
         if store is not None and not args.no_stall:
