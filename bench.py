@@ -65,18 +65,48 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML
+    polled every 10 ms on a thread (the value leg lasts ~80 ms, too short for
+    nvidia-smi's 100 ms floor), nvidia-smi -lms 100 when NVML is missing."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_s: float = 0.01):
         self.gpu = gpu_index
+        self.period = period_s
         self.proc = None
         self.lines = []
+        self.samples = []            # (sm_mhz, max_mhz, set of reasons)
+        self._stop = threading.Event()
+        self._t = None
+        self.source = "none"
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def poll():
+                while not self._stop.is_set():
+                    sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, mx, {k for k, b in bits.items() if r & b}))
+                    self._stop.wait(self.period)
+            self._t = threading.Thread(target=poll, daemon=True)
+            self._t.start()
+            self.source = "nvml, 10 ms"
+            return self
+        except Exception:  # noqa: BLE001 - fall back to nvidia-smi
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
@@ -84,6 +114,7 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            self.source = "nvidia-smi, 100 ms"
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -100,24 +131,26 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        elif self._t is not None:
+            self._stop.set()
+            self._t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        samples = list(self.samples)
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
+                samples.append((float(f[1]), float(f[2]),
+                                {n for n, v in zip(self.NAMES, f[5:9]) if v.lower() == "active"}))
             except ValueError:
                 continue
-            for name, val in zip(names, f[5:9]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [x[0] for x in samples]
+        reasons = set().union(*[x[2] for x in samples]) if samples else set()
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": samples[-1][1] if samples else None,
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
 def dist_backend() -> str:
@@ -1003,8 +1036,10 @@ def run_b200(args):
                   file=sys.stderr)
         if args.stall_no_persist:
             ck.set_persist(False)
-        stall = measure_stall(ck, arena, dev, i_ckpt, args.stall_checkpoints, args.fb_ms,
-                              args.stall_rounds, world, rank)
+        with ClockSampler(local, period_s=0.1) as stall_clk:
+            stall = measure_stall(ck, arena, dev, i_ckpt, args.stall_checkpoints, args.fb_ms,
+                                  args.stall_rounds, world, rank)
+        stall["clocks"] = stall_clk.summary()
         stall["persist_tier"] = "off (diagnostic)" if args.stall_no_persist else \
             (f"off ({persist_dropped})" if persist_dropped else
              ("on" if store is not None else "none configured"))
