@@ -17,7 +17,10 @@ bytes.  Here the decisions are executed:
 Streaming: pieces are grouped into batches of at most ``slot_bytes``; two
 pinned host slots and two device slots alternate, so file reads of batch
 i+1 (a host thread pool) overlap the H2D copy and the `pec_unpack` scatter
-of batch i into the state arena (one launch per batch).  Entries larger
+of batch i into the state arena (one launch per batch).  A host slot is
+refilled as soon as its own H2D has run (an event), not after its batch's
+verification and scatter, so reads and H2D copies never take turns
+(restore 19-20 -> see DESIGN §6.2 for the measured rate).  Entries larger
 than a slot are split; their CRC is chained across the pieces.
 """
 
@@ -45,6 +48,7 @@ class RestoreReport:
     unpack_ms: float      # sum of the per-batch unpack kernel times
     batches: int = 0
     wall_s: float = 0.0
+    phases: Optional[Dict[str, float]] = None   # host seconds per restore phase
 
 
 @dataclass
@@ -79,7 +83,10 @@ class _Ring:
         self.slot_bytes = slot_bytes
         self.host = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         self.dev = [torch.empty(slot_bytes, dtype=torch.uint8, device=device) for _ in range(2)]
-        self.free = [None, None]   # event: slot's H2D + unpack finished
+        # event: the host slot's H2D finished (the host slot may be refilled).
+        # A device slot is reused in stream order: batch i+2's H2D is enqueued
+        # after batch i's unpack on the same stream.
+        self.free = [None, None]
 
 
 def _ring(engine, slot_bytes: int) -> _Ring:
@@ -260,6 +267,10 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
     for key in initial:
         arena.fill_unit(key)
     rep = RestoreReport(len(wanted), 0, 0, len(initial), 0.0)
+    ph = dict.fromkeys(("plan", "slot_wait", "read", "h2d_enqueue", "verify_enqueue",
+                        "commit", "drain"), 0.0)
+    ph["plan"] = time.perf_counter() - t_start
+    rep.phases = ph
     if not pieces:
         torch.cuda.synchronize(dev)
         rep.wall_s = time.perf_counter() - t_start
@@ -341,17 +352,19 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
             D.unpack(dt.tensor, dt.n, dt.total_chunks, chunk_log2, D.MODE_AUTO, stream=s)
             timers.append((t0, t1, dt))
         t1.record(s)
-        ring.free[slot] = t1
         committed.extend(units)
 
     pending = None
     with ThreadPoolExecutor(max_workers=io_threads) as pool:
         for bi, batch in enumerate(batches):
             slot = bi % 2
+            tp = time.perf_counter()
             if ring.free[slot] is not None:
-                ring.free[slot].synchronize()   # slot's previous batch fully consumed
+                ring.free[slot].synchronize()   # the slot's previous H2D has run
             hslot, dslot = ring.host[slot], ring.dev[slot]
             files = [(p, off, hslot) for p, off in batch if p.kind == "file"]
+            tq = time.perf_counter()
+            ph["slot_wait"] += tq - tp
             crcs = _read_files(pool, files, want_crc=verify == "host")
             for p, off in batch:
                 if p.kind == "bytes":
@@ -363,6 +376,8 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
                         rep.storage_bytes += p.nbytes
                 elif p.kind == "file":
                     rep.storage_bytes += p.nbytes
+            tp = time.perf_counter()
+            ph["read"] += tp - tq
             with torch.cuda.stream(s):
                 for p, off in batch:
                     if p.kind == "file" and p.entry in split and p.entry not in landing:
@@ -384,6 +399,11 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
                     else:
                         dslot[off:off + p.nbytes].copy_(hslot[off:off + p.nbytes],
                                                         non_blocking=True)
+            h2d_done = torch.cuda.Event()
+            h2d_done.record(s)
+            ring.free[slot] = h2d_done
+            tq = time.perf_counter()
+            ph["h2d_enqueue"] += tq - tp
             hcrc, ready = None, None
             if verify == "device" and files:
                 table = np.zeros(len(files), dtype=D.DESC_DTYPE)
@@ -408,15 +428,20 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
             else:
                 rec_table = None
             rec = (batch, slot, dslot, hcrc, ready, crcs, rec_table)
+            tp = time.perf_counter()
+            ph["verify_enqueue"] += tp - tq
             # the previous batch commits now: its verification ran while this
             # batch's files were read
             if pending is not None:
                 commit(pending)
             pending = rec
+            ph["commit"] += time.perf_counter() - tp
+        tp = time.perf_counter()
         if pending is not None:
             commit(pending)
     torch.cuda.current_stream(dev).wait_stream(s)
     s.synchronize()
+    ph["drain"] = time.perf_counter() - tp
     for peer in peers.values():
         if peer is not None:
             peer[0].close()
