@@ -19,8 +19,9 @@ pinned host slots and two device slots alternate, so file reads of batch
 i+1 (a host thread pool) overlap the H2D copy and the `pec_unpack` scatter
 of batch i into the state arena (one launch per batch).  A host slot is
 refilled as soon as its own H2D has run (an event), not after its batch's
-verification and scatter, so reads and H2D copies never take turns
-(restore 19-20 -> see DESIGN §6.2 for the measured rate).  Entries larger
+verification and scatter, so reads and H2D copies never take turns (they
+did: 19-20 GB/s; now 36.6 GB/s for 26.1 GB, the reads at ~42 GB/s being the
+bound).  Entries larger
 than a slot are split; their CRC is chained across the pieces.
 """
 
