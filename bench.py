@@ -897,6 +897,24 @@ def run_b200(args):
             store = None
             ck.engine.store = None
             fit = fit_np
+    if store is not None and persist == "shm":
+        # the tmpfs itself may be smaller than RAM (container /dev/shm limits)
+        try:
+            st_ = os.statvfs(str(store.root))
+            shm_free = st_.f_bavail * st_.f_frsize
+        except OSError:
+            shm_free = None
+        local_n = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+        short = shm_free is not None and shm_free < 1.05 * shm_versions * shard * local_n
+        if max_over_ranks(1.0 if short else 0.0, world, dev) > 0:
+            shm_free = shm_free or 0
+            print(f"bench: /dev/shm has {shm_free / 1e9:.0f} GB free, the persist tier needs "
+                  f"{shm_versions} versions x {local_n} ranks x {shard / 1e9:.1f} GB; "
+                  "persist tier off", file=sys.stderr)
+            persist_dropped = f"/dev/shm: {shm_free / 1e9:.0f} GB free for {local_n} ranks"
+            store = None
+            ck.engine.store = None
+            fit = host_buffers_that_fit(eng.staging.numel(), 3)
     n_host = int(min_over_ranks(float(fit), world, dev))    # node-wide minimum
     pin_error = None
     if n_host < 2:
