@@ -238,7 +238,7 @@ def _chain(running: Dict[str, int], p: "_Piece", crc: int) -> None:
 
 def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
             chunk_log2: int = D.DEFAULT_CHUNK_LOG2, stream=None,
-            slot_bytes: int = 256 << 20, io_threads: int = 16,
+            slot_bytes: int = 256 << 20, io_threads: Optional[int] = None,
             verify: str = "device") -> RestoreReport:
     """Execute ``plan`` for the units resident in ``engine.arena`` (or the
     given subset ``keys``).  ``engine`` is a DeviceCheckpointEngine whose
@@ -257,6 +257,8 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
     restored (from verified bytes) when it was raised."""
     if verify not in ("device", "host"):
         raise ValueError("verify must be 'device' or 'host'")
+    if io_threads is None:          # one reader per usable core
+        io_threads = max(4, len(os.sched_getaffinity(0)))
     import time
     import torch
     t_start = time.perf_counter()

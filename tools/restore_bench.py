@@ -60,7 +60,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--verify", default="device", choices=["device", "host"])
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--io-threads", type=int, default=16)
+    ap.add_argument("--io-threads", type=int, default=None, help="default: one per core")
     ap.add_argument("--slot-mb", type=int, default=256)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -95,7 +95,8 @@ def main():
                             "unpack_ms": round(rep.unpack_ms, 2),
                             "phases_s": {k: round(v, 3) for k, v in (rep.phases or {}).items()},
                             "bit_identical": ok})
-    out["read_ceiling_GBps"] = read_ceiling(store, version, args.io_threads, args.slot_mb << 20)
+    import os
+    out["read_ceiling_GBps"] = read_ceiling(store, version, args.io_threads or max(4, len(os.sched_getaffinity(0))), args.slot_mb << 20)
     ck.close()
     shutil.rmtree(root, ignore_errors=True)
     print(json.dumps(out))
