@@ -14,6 +14,7 @@ read ceiling measured with the same reader (`restore._read_files`) alone.
 """
 
 import json
+import os
 import shutil
 import sys
 import time
@@ -95,8 +96,8 @@ def main():
                             "unpack_ms": round(rep.unpack_ms, 2),
                             "phases_s": {k: round(v, 3) for k, v in (rep.phases or {}).items()},
                             "bit_identical": ok})
-    import os
-    out["read_ceiling_GBps"] = read_ceiling(store, version, args.io_threads or max(4, len(os.sched_getaffinity(0))), args.slot_mb << 20)
+    threads = args.io_threads or max(4, len(os.sched_getaffinity(0)))
+    out["read_ceiling_GBps"] = read_ceiling(store, version, threads, args.slot_mb << 20)
     ck.close()
     shutil.rmtree(root, ignore_errors=True)
     print(json.dumps(out))
