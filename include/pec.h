@@ -33,6 +33,7 @@ extern "C" {
 #define PEC_E_CUDA (-2)    /* CUDA launch or runtime error (maps to RuntimeError)   */
 #define PEC_E_RANGE (-3)   /* size exceeds a kernel limit (e.g. experts > 4096)     */
 #define PEC_E_IO (-4)      /* file I/O failed (maps to OSError)                      */
+#define PEC_E_CRASH (-5)   /* injected crash: write budget exhausted (CrashPoint)    */
 
 #define PEC_ABI_VERSION 1
 
@@ -198,6 +199,20 @@ int pec_crc32c_many(const void* base, const uint64_t* offs,
  * open/write/fsync/truncate/close failure. */
 int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
                     int n, uint32_t* crc_out, int threads, int flags);
+
+/* Crash injection on the native writer.
+ * Replaces: TruncatingInjector.write over the entry-file loop
+ * (store.py:124-146, 210-216).  *budget bytes are spent in the given file
+ * order as the sequential writer spends them: every file that fits is
+ * written whole; the first that does not keeps its first *budget bytes and
+ * the files after it are not created; *budget is left at the bytes unspent
+ * and PEC_E_CRASH is returned (PEC_OK when every file fit).  The surviving
+ * prefix is written by the same parallel pool as pec_write_files, so the
+ * partial tree is identical to the sequential writer's.  crc_out (may be
+ * NULL) is filled only on PEC_OK. */
+int pec_write_files_budget(const char* const* paths, const void* const* bufs,
+                           const uint64_t* lens, int n, uint32_t* crc_out, int threads,
+                           int flags, uint64_t* budget);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -260,12 +260,40 @@ int pec_crc32c_many(const void* base, const uint64_t* offs, const uint64_t* lens
 //   launch thread for host cores (the caller's own thread is not touched).
 // flags bit 3: overwrite existing files in place (recycled files, see
 //   DiskStore(recycle=True)) instead of truncating them first.
-int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
-                    int n, uint32_t* crc_out, int threads, int flags) {
-  if (n < 0 || (n > 0 && (paths == nullptr || bufs == nullptr || lens == nullptr)))
+static int write_files_impl(const char* const* paths, const void* const* bufs,
+                            const uint64_t* full_lens, int n, uint32_t* crc_out, int threads,
+                            int flags, uint64_t* budget) {
+  if (n < 0 || (n > 0 && (paths == nullptr || bufs == nullptr || full_lens == nullptr)))
     return PEC_E_INVAL;
   if (n == 0) return PEC_OK;
   if (threads < 1) threads = 1;
+  // crash injection: the byte budget is spent in the given file order, as a
+  // sequential writer would spend it (TruncatingInjector, store.py:124-146):
+  // the file that exhausts it keeps its first bytes, later files are never
+  // created.  The surviving prefix is then written by the parallel pool, so
+  // the partial tree equals the sequential writer's.
+  int n_files = n;
+  bool crashed = false;
+  std::vector<uint64_t> cut;
+  const uint64_t* lens = full_lens;
+  if (budget != nullptr) {
+    cut.assign(full_lens, full_lens + n);
+    uint64_t left = *budget;
+    for (int i = 0; i < n; ++i) {
+      if (full_lens[i] <= left) {
+        left -= full_lens[i];
+        continue;
+      }
+      cut[i] = left;
+      left = 0;
+      crashed = true;
+      n_files = i + 1;
+      break;
+    }
+    *budget = left;
+    lens = cut.data();
+  }
+  n = n_files;
   constexpr uint64_t kPiece = 4ull << 20;
   constexpr uint64_t kBlock = 4096;
   constexpr uint64_t kRange = 64ull << 20;
@@ -381,6 +409,7 @@ int pec_write_files(const char* const* paths, const void* const* bufs, const uin
   for (int t = 0; t < nt; ++t) pool.emplace_back(work);
   for (auto& th : pool) th.join();
   if (failed.load()) return PEC_E_IO;
+  if (crashed) return PEC_E_CRASH;
   if (crc_out != nullptr) {
     // ranges of a file are consecutive items (planned in file order)
     size_t k = 0;
@@ -393,6 +422,18 @@ int pec_write_files(const char* const* paths, const void* const* bufs, const uin
     }
   }
   return PEC_OK;
+}
+
+int pec_write_files(const char* const* paths, const void* const* bufs, const uint64_t* lens,
+                    int n, uint32_t* crc_out, int threads, int flags) {
+  return write_files_impl(paths, bufs, lens, n, crc_out, threads, flags, nullptr);
+}
+
+int pec_write_files_budget(const char* const* paths, const void* const* bufs,
+                           const uint64_t* lens, int n, uint32_t* crc_out, int threads,
+                           int flags, uint64_t* budget) {
+  if (budget == nullptr) return PEC_E_INVAL;
+  return write_files_impl(paths, bufs, lens, n, crc_out, threads, flags, budget);
 }
 
 }  // extern "C"

@@ -759,6 +759,7 @@ const char* pec_strerror(int code) {
     case PEC_E_CUDA: return "CUDA launch/runtime error";
     case PEC_E_RANGE: return "size exceeds a kernel limit";
     case PEC_E_IO: return "file I/O failed";
+    case PEC_E_CRASH: return "injected crash: write budget exhausted";
     default: return "unknown error";
   }
 }

@@ -27,6 +27,7 @@ PEC_E_INVAL = -1
 PEC_E_CUDA = -2
 PEC_E_RANGE = -3
 PEC_E_IO = -4
+PEC_E_CRASH = -5
 
 # numpy mirror of `pec_copy_desc`
 DESC_DTYPE = np.dtype([("src", "<u8"), ("dst", "<u8"), ("nbytes", "<u8"),
@@ -84,6 +85,7 @@ def _load():
         "pec_crc32c_combine": (c_u32, [c_u32, c_u32, c_u64]),
         "pec_crc32c_many": (c_int, [vp, vp, vp, c_int, vp, c_int]),
         "pec_write_files": (c_int, [vp, vp, vp, c_int, vp, c_int, c_int]),
+        "pec_write_files_budget": (c_int, [vp, vp, vp, c_int, vp, c_int, c_int, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -106,7 +108,8 @@ def exported_symbols():
             "pec_select_sequential",
             "pec_select_load_aware", "pec_pack", "pec_unpack", "pec_plan_chunks",
             "pec_expand_plan", "pec_pack_indirect", "pec_pack_crc", "pec_crc_device",
-            "pec_crc32c", "pec_crc32c_combine", "pec_crc32c_many", "pec_write_files"]
+            "pec_crc32c", "pec_crc32c_combine", "pec_crc32c_many", "pec_write_files",
+            "pec_write_files_budget"]
 
 
 def _check(rc: int, what: str) -> None:
@@ -356,13 +359,17 @@ def crc32c_many(base, offsets, lengths, threads: Optional[int] = None) -> np.nda
 
 def write_files(paths, buffers, threads: Optional[int] = None, want_crc: bool = True,
                 fsync: bool = False, direct: bool = False, background: bool = False,
-                overwrite: bool = False):
+                overwrite: bool = False, budget: Optional[int] = None):
     """Native multi-threaded writer (pec_write_files): file i <- buffers[i]
     (bytes-like / ndarray / CPU tensor).  Returns the CRC-32C of each file
     (uint32 ndarray) when ``want_crc``.  ``direct`` opens files O_DIRECT
     (page-cache bypass; buffered where the filesystem refuses it; large files
     range-parallel); ``background`` runs the writer threads at nice +10;
-    ``overwrite`` rewrites existing files in place (recycled files)."""
+    ``overwrite`` rewrites existing files in place (recycled files).
+
+    ``budget`` (crash injection, pec_write_files_budget): at most that many
+    bytes are written, spent in file order like the sequential writer; then
+    the return value is ``(crcs or None, bytes_left, crashed)``."""
     n = len(paths)
     keep = [_host_buffer(b) for b in buffers]
     c_paths = (ctypes.c_char_p * n)(*[os.fsencode(str(p)) for p in paths])
@@ -371,12 +378,19 @@ def write_files(paths, buffers, threads: Optional[int] = None, want_crc: bool = 
     out = np.zeros(n, dtype=np.uint32) if want_crc else None
     if threads is None:
         threads = max(1, len(os.sched_getaffinity(0)))
-    rc = lib().pec_write_files(ctypes.cast(c_paths, ctypes.c_void_p),
-                               ctypes.cast(c_bufs, ctypes.c_void_p),
-                               lens.ctypes.data if n else None, n,
-                               out.ctypes.data if want_crc and n else None, int(threads),
-                               (1 if fsync else 0) | (2 if direct else 0) |
-                               (4 if background else 0) | (8 if overwrite else 0))
-    _check(rc, "pec_write_files")
+    flags = (1 if fsync else 0) | (2 if direct else 0) | (4 if background else 0) | \
+        (8 if overwrite else 0)
+    args = (ctypes.cast(c_paths, ctypes.c_void_p), ctypes.cast(c_bufs, ctypes.c_void_p),
+            lens.ctypes.data if n else None, n, out.ctypes.data if want_crc and n else None,
+            int(threads), flags)
+    if budget is None:
+        rc = lib().pec_write_files(*args)
+        _check(rc, "pec_write_files")
+        del keep
+        return out
+    left = np.array([max(0, int(budget))], dtype=np.uint64)
+    rc = lib().pec_write_files_budget(*args, left.ctypes.data)
+    if rc != PEC_E_CRASH:
+        _check(rc, "pec_write_files_budget")
     del keep
-    return out
+    return (out if rc == PEC_OK else None), int(left[0]), rc == PEC_E_CRASH

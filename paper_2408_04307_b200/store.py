@@ -259,14 +259,22 @@ class DiskStore:
             (vdir / f"rank{r:04d}").mkdir(parents=True, exist_ok=True)
         given = crcs is not None and payloads is not None and \
             all(e.store_key in crcs for e in entries)
-        if injector is None and payloads is not None and entries:
+        if entries and (injector is None or type(injector) is TruncatingInjector):
             # native writer: threads take whole files (largest first) and CRC
-            # each 4 MiB piece right after writing it
+            # each 4 MiB piece right after writing it.  A TruncatingInjector's
+            # byte budget is spent natively in entry order, exactly as the
+            # sequential loop below spends it (pec_write_files_budget)
             paths = [vdir / _entry_path(e.rank, e.store_key) for e in entries]
             reused = self._adopt_spares(entries, data, paths) if self.recycle else 0
-            got = _dev.write_files(paths, data, threads=self.io_threads, want_crc=not given,
-                                   fsync=self.fsync, direct=self.direct_io,
-                                   background=self.background, overwrite=reused > 0)
+            kw = dict(threads=self.io_threads, want_crc=not given, fsync=self.fsync,
+                      direct=self.direct_io, background=self.background, overwrite=reused > 0)
+            if injector is None:
+                got = _dev.write_files(paths, data, **kw)
+            else:
+                got, injector.remaining, crashed = _dev.write_files(
+                    paths, data, budget=injector.remaining, **kw)
+                if crashed:
+                    raise CrashPoint("write budget exhausted")
             crc_list = [crcs[e.store_key] for e in entries] if given else [int(c) for c in got]
             return [(e.store_key, _entry_path(e.rank, e.store_key), _nbytes(p), c)
                     for e, p, c in zip(entries, data, crc_list)]

@@ -324,3 +324,47 @@ def test_retire_recycles_files_without_changing_what_readers_see(tmp_path, recyc
     st.trim_spares([0, 1], keep_bytes=0)
     assert not any(p.is_file() for p in (tmp_path / "s").rglob("*.bin") if ".spare" in str(p))
     assert os.listdir(tmp_path / "s")  # the store itself remains
+
+
+class _SequentialInjector(TruncatingInjector):
+    """Same budget semantics, but (not being a TruncatingInjector itself)
+    routes the store through its sequential Python write loop."""
+
+
+@pytest.mark.parametrize("direct", [False, True])
+def test_native_writer_crash_budget_matches_the_sequential_writer(tmp_path, direct):
+    """Crash injection on the native parallel writer (pec_write_files_budget):
+    at budgets before, inside and after every file boundary, real multi-MiB
+    payloads of several ranks leave the byte-identical partial tree, the same
+    CrashPoint and the same unspent budget as the sequential writer loop
+    (TruncatingInjector semantics, reference store.py:124-146)."""
+    rng = np.random.default_rng(11)
+    sizes = [0, 3 << 20, 1, (5 << 20) + 7, 4096, 700_001, 2 << 20]
+    ents = [StoreEntry(f"ew.L{i}.E{i % 3}", i % 3, f"ew.L{i}.E{i % 3}", 0, n)
+            for i, n in enumerate(sizes)]
+    pay = {e.store_key: rng.bytes(e.stop - e.start) for e in ents}
+    order = [e.stop - e.start for e in sorted(ents)]
+    edges = np.cumsum(order)
+    total = DiskStore(tmp_path / "probe").serialized_size(1, 5, 0, ents, payloads=pay)
+    budgets = sorted({0, 1, total - 1, total, total + 5} |
+                     {int(x) + d for x in edges for d in (-1, 0, 1) if x + d >= 0})
+    for b in budgets:
+        outs, trees = [], []
+        for name, inj_cls, threads in (("native", TruncatingInjector, 4),
+                                       ("seq", _SequentialInjector, 1)):
+            root = tmp_path / f"{name}{b}"
+            st = DiskStore(root, io_threads=threads, direct_io=direct)
+            inj = inj_cls(b)
+            try:
+                st.write_version(1, 5, 0, ents, injector=inj, payloads=pay)
+                res = "ok"
+            except CrashPoint:
+                res = "crash"
+            outs.append((res, inj.remaining, st.complete_versions()))
+            trees.append({str(p.relative_to(root)): p.read_bytes()
+                          for p in sorted(root.rglob("*")) if p.is_file()})
+        assert outs[0] == outs[1], b
+        assert trees[0] == trees[1], b
+    ok = DiskStore(tmp_path / "full", io_threads=4, direct_io=direct)
+    ok.write_version(1, 5, 0, ents, injector=TruncatingInjector(total + 1), payloads=pay)
+    assert ok.load_checkpoint(1) == pay
