@@ -358,90 +358,99 @@ def restore(engine, plan: RecoveryPlan, keys: Optional[Iterable[str]] = None,
         committed.extend(units)
 
     pending = None
-    with ThreadPoolExecutor(max_workers=io_threads) as pool:
-        for bi, batch in enumerate(batches):
-            slot = bi % 2
-            tp = time.perf_counter()
-            if ring.free[slot] is not None:
-                ring.free[slot].synchronize()   # the slot's previous H2D has run
-            hslot, dslot = ring.host[slot], ring.dev[slot]
-            files = [(p, off, hslot) for p, off in batch if p.kind == "file"]
-            tq = time.perf_counter()
-            ph["slot_wait"] += tq - tp
-            crcs = _read_files(pool, files, want_crc=verify == "host")
-            for p, off in batch:
-                if p.kind == "bytes":
-                    hslot.numpy()[off:off + p.nbytes] = np.frombuffer(
-                        p.host, dtype=np.uint8)[p.host_off:p.host_off + p.nbytes]
-                    if p.entry is None and plan.decisions[p.unit].source == "memory":
-                        rep.memory_bytes += p.nbytes
-                    else:
+    try:
+        with ThreadPoolExecutor(max_workers=io_threads) as pool:
+            for bi, batch in enumerate(batches):
+                slot = bi % 2
+                tp = time.perf_counter()
+                if ring.free[slot] is not None:
+                    ring.free[slot].synchronize()   # the slot's previous H2D has run
+                hslot, dslot = ring.host[slot], ring.dev[slot]
+                files = [(p, off, hslot) for p, off in batch if p.kind == "file"]
+                tq = time.perf_counter()
+                ph["slot_wait"] += tq - tp
+                crcs = _read_files(pool, files, want_crc=verify == "host")
+                for p, off in batch:
+                    if p.kind == "bytes":
+                        hslot.numpy()[off:off + p.nbytes] = np.frombuffer(
+                            p.host, dtype=np.uint8)[p.host_off:p.host_off + p.nbytes]
+                        if p.entry is None and plan.decisions[p.unit].source == "memory":
+                            rep.memory_bytes += p.nbytes
+                        else:
+                            rep.storage_bytes += p.nbytes
+                    elif p.kind == "file":
                         rep.storage_bytes += p.nbytes
-                elif p.kind == "file":
-                    rep.storage_bytes += p.nbytes
-            tp = time.perf_counter()
-            ph["read"] += tp - tq
-            with torch.cuda.stream(s):
-                for p, off in batch:
-                    if p.kind == "file" and p.entry in split and p.entry not in landing:
-                        # a device buffer for the whole entry, allocated on s (reused in
-                        # stream order once its scatter has run)
-                        lo = arena.slot(p.unit).offset + p.start - p.file_off
-                        buf = torch.empty(p.entry_size + STAGE_ALIGN, dtype=torch.uint8,
-                                          device=dev)
-                        landing[p.entry] = (buf, (lo - buf.data_ptr()) % STAGE_ALIGN)
-                for p, off in batch:
-                    if p.kind == "host":
-                        dslot[off:off + p.nbytes].copy_(p.host[p.host_off:p.host_off + p.nbytes],
-                                                        non_blocking=True)
-                        rep.memory_bytes += p.nbytes
-                    elif p.kind == "file" and p.entry in split:
-                        buf, base = landing[p.entry]
-                        o = base + p.file_off
-                        buf[o:o + p.nbytes].copy_(hslot[off:off + p.nbytes], non_blocking=True)
-                    else:
-                        dslot[off:off + p.nbytes].copy_(hslot[off:off + p.nbytes],
-                                                        non_blocking=True)
-            h2d_done = torch.cuda.Event()
-            h2d_done.record(s)
-            ring.free[slot] = h2d_done
-            tq = time.perf_counter()
-            ph["h2d_enqueue"] += tq - tp
-            hcrc, ready = None, None
-            if verify == "device" and files:
-                table = np.zeros(len(files), dtype=D.DESC_DTYPE)
-                for i, (p, off, _) in enumerate(files):
-                    table[i] = (dev_src(p, dslot, off), 0, p.nbytes, 0)
-                nchunks = D.plan_chunks(table, chunk_log2)
-                dt = DeviceTable(table, nchunks, dev, chunk_log2)
-                need = D.crc_scratch_words(nchunks)
-                sc = crc_scratch.get(slot)
-                if sc is None or sc[0].numel() < need or sc[1].numel() < len(files):
-                    sc = (torch.empty(need, dtype=torch.int32, device=dev),
-                          torch.empty(max(len(files), 1), dtype=torch.int32, device=dev))
-                    crc_scratch[slot] = sc
-                D.crc_device(dt.tensor, dt.n, dt.total_chunks, sc[0], sc[1], chunk_log2, stream=s)
-                hcrc = crc_host[crc_pos:crc_pos + dt.n]
-                crc_pos += dt.n
+                tp = time.perf_counter()
+                ph["read"] += tp - tq
                 with torch.cuda.stream(s):
-                    hcrc.copy_(sc[1][:dt.n], non_blocking=True)
-                ready = torch.cuda.Event()
-                ready.record(s)
-                rec_table = dt     # alive until the batch commits (after `ready`)
-            else:
-                rec_table = None
-            rec = (batch, slot, dslot, hcrc, ready, crcs, rec_table)
+                    for p, off in batch:
+                        if p.kind == "file" and p.entry in split and p.entry not in landing:
+                            # a device buffer for the whole entry, allocated on s (reused in
+                            # stream order once its scatter has run)
+                            lo = arena.slot(p.unit).offset + p.start - p.file_off
+                            buf = torch.empty(p.entry_size + STAGE_ALIGN, dtype=torch.uint8,
+                                              device=dev)
+                            landing[p.entry] = (buf, (lo - buf.data_ptr()) % STAGE_ALIGN)
+                    for p, off in batch:
+                        if p.kind == "host":
+                            dslot[off:off + p.nbytes].copy_(p.host[p.host_off:p.host_off + p.nbytes],
+                                                            non_blocking=True)
+                            rep.memory_bytes += p.nbytes
+                        elif p.kind == "file" and p.entry in split:
+                            buf, base = landing[p.entry]
+                            o = base + p.file_off
+                            buf[o:o + p.nbytes].copy_(hslot[off:off + p.nbytes], non_blocking=True)
+                        else:
+                            dslot[off:off + p.nbytes].copy_(hslot[off:off + p.nbytes],
+                                                            non_blocking=True)
+                h2d_done = torch.cuda.Event()
+                h2d_done.record(s)
+                ring.free[slot] = h2d_done
+                tq = time.perf_counter()
+                ph["h2d_enqueue"] += tq - tp
+                hcrc, ready = None, None
+                if verify == "device" and files:
+                    table = np.zeros(len(files), dtype=D.DESC_DTYPE)
+                    for i, (p, off, _) in enumerate(files):
+                        table[i] = (dev_src(p, dslot, off), 0, p.nbytes, 0)
+                    nchunks = D.plan_chunks(table, chunk_log2)
+                    dt = DeviceTable(table, nchunks, dev, chunk_log2)
+                    need = D.crc_scratch_words(nchunks)
+                    sc = crc_scratch.get(slot)
+                    if sc is None or sc[0].numel() < need or sc[1].numel() < len(files):
+                        sc = (torch.empty(need, dtype=torch.int32, device=dev),
+                              torch.empty(max(len(files), 1), dtype=torch.int32, device=dev))
+                        crc_scratch[slot] = sc
+                    D.crc_device(dt.tensor, dt.n, dt.total_chunks, sc[0], sc[1], chunk_log2, stream=s)
+                    hcrc = crc_host[crc_pos:crc_pos + dt.n]
+                    crc_pos += dt.n
+                    with torch.cuda.stream(s):
+                        hcrc.copy_(sc[1][:dt.n], non_blocking=True)
+                    ready = torch.cuda.Event()
+                    ready.record(s)
+                    rec_table = dt     # alive until the batch commits (after `ready`)
+                else:
+                    rec_table = None
+                rec = (batch, slot, dslot, hcrc, ready, crcs, rec_table)
+                tp = time.perf_counter()
+                ph["verify_enqueue"] += tp - tq
+                # the previous batch commits now: its verification ran while this
+                # batch's files were read
+                if pending is not None:
+                    commit(pending)
+                pending = rec
+                ph["commit"] += time.perf_counter() - tp
             tp = time.perf_counter()
-            ph["verify_enqueue"] += tp - tq
-            # the previous batch commits now: its verification ran while this
-            # batch's files were read
             if pending is not None:
                 commit(pending)
-            pending = rec
-            ph["commit"] += time.perf_counter() - tp
-        tp = time.perf_counter()
-        if pending is not None:
-            commit(pending)
+    except BaseException:
+        # a failed restore (e.g. ChecksumMismatchError) must not leave H2D copies or
+        # scatters in flight on the ring's slots: the next restore reuses them
+        s.synchronize()
+        for peer in peers.values():
+            if peer is not None:
+                peer[0].close()
+        raise
     torch.cuda.current_stream(dev).wait_stream(s)
     s.synchronize()
     ph["drain"] = time.perf_counter() - tp
