@@ -237,6 +237,17 @@ SHM_VERSIONS_IN_FLIGHT = 3
 PERSIST_PROBE_VERSIONS = 3
 
 
+def tmpfs_room(root, need_bytes: int, margin: float = 1.05):
+    """(free bytes, too small?) of the filesystem holding ``root`` for
+    ``need_bytes`` (+5 %) of persist versions; (None, False) when unknown."""
+    try:
+        st = os.statvfs(str(root))
+    except OSError:
+        return None, False
+    free = st.f_bavail * st.f_frsize
+    return free, free < margin * need_bytes
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -899,13 +910,8 @@ def run_b200(args):
             fit = fit_np
     if store is not None and persist == "shm":
         # the tmpfs itself may be smaller than RAM (container /dev/shm limits)
-        try:
-            st_ = os.statvfs(str(store.root))
-            shm_free = st_.f_bavail * st_.f_frsize
-        except OSError:
-            shm_free = None
         local_n = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
-        short = shm_free is not None and shm_free < 1.05 * shm_versions * shard * local_n
+        shm_free, short = tmpfs_room(store.root, shm_versions * shard * local_n)
         if max_over_ranks(1.0 if short else 0.0, world, dev) > 0:
             shm_free = shm_free or 0
             print(f"bench: /dev/shm has {shm_free / 1e9:.0f} GB free, the persist tier needs "

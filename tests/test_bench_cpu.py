@@ -96,3 +96,15 @@ def test_multirank_retention_bounds_the_store(tmp_path):
         assert int(worst) <= 4
         assert int(tot) <= (4 + int(recycle)) * one_version
         assert complete.strip() == "[24]"
+
+
+def test_tmpfs_room_flags_a_filesystem_too_small_for_the_versions(tmp_path):
+    """The persist tier is dropped (and the line says so) when the store's
+    filesystem cannot hold the versions in flight for every local rank."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    free, short = bench.tmpfs_room(tmp_path, 1)
+    assert free > 0 and short is False
+    free, short = bench.tmpfs_room(tmp_path, free * 2)
+    assert short is True
+    assert bench.tmpfs_room(tmp_path / "missing" / "dir", 1) == (None, False)
