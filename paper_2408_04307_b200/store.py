@@ -215,6 +215,7 @@ class DiskStore:
         self.recycle = recycle
         self._spares: Dict[int, Dict[int, List[Path]]] = {}   # rank -> size -> files
         self._spare_lock = threading.Lock()
+        self.recycled_files = 0      # entry files written over a retired version's file
 
     def version_dir(self, version: int) -> Path:
         return self.root / f"v{version:06d}"
@@ -305,6 +306,7 @@ class DiskStore:
                 if pool:
                     os.replace(pool.pop(), path)
                     n += 1
+            self.recycled_files += n
         return n
 
     def retire(self, version: int, ranks: Optional[Iterable[int]] = None,

@@ -30,10 +30,12 @@ def _mutate(arena, step):
         v[:: 97].add_(step + 1)
 
 
-@pytest.mark.parametrize("drain_first", [None, 100_003])
-def test_toy_sequential_chain_persists_exact_bytes(dev, tmp_path, drain_first):
+@pytest.mark.parametrize("drain_first,recycle", [(None, False), (100_003, False), (None, True)])
+def test_toy_sequential_chain_persists_exact_bytes(dev, tmp_path, drain_first, recycle):
     """drain_first=100_003: the pipelined drain splits every pack at odd
-    staging offsets (~8 segments, rows cut mid-copy, unaligned pieces)."""
+    staging offsets (~8 segments, rows cut mid-copy, unaligned pieces).
+    recycle: superseded versions are retired during the chain and later
+    versions overwrite their files in place; what remains is exact."""
     import torch
     from paper_2408_04307_b200 import configs
     from paper_2408_04307_b200.arena import StateArena
@@ -42,7 +44,7 @@ def test_toy_sequential_chain_persists_exact_bytes(dev, tmp_path, drain_first):
     w = configs.toy()
     layout = w.layout()
     arena = StateArena(layout, [0], dev, w.expert_tensors)
-    store = DiskStore(tmp_path)
+    store = DiskStore(tmp_path, recycle=recycle)
     ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=5)
     if drain_first is not None:
         ck.engine.drain_first = drain_first
@@ -61,9 +63,16 @@ def test_toy_sequential_chain_persists_exact_bytes(dev, tmp_path, drain_first):
             expected[buf.version] = (_expected_entries(arena.buffer.cpu().numpy(), arena,
                                                        buf.content, [0]), buf.iteration)
             ck.wait_pack()  # next update must not race the pack
+            if recycle:
+                for old in store.complete_versions()[:-1]:
+                    store.retire(old)
     ck.finish()
     versions = store.complete_versions()
-    assert versions == sorted(expected)
+    if recycle:
+        assert versions and set(versions) <= set(expected) and versions[-1] == max(expected)
+        assert store.recycled_files > 0
+    else:
+        assert versions == sorted(expected)
     for v in versions:
         got = store.load_checkpoint(v)
         want, it = expected[v]
