@@ -1064,6 +1064,8 @@ def run_b200(args):
             stall = measure_stall(ck, arena, dev, i_ckpt, args.stall_checkpoints, args.fb_ms,
                                   args.stall_rounds, world, rank)
         stall["clocks"] = stall_clk.summary()
+        if store is not None and getattr(store, "recycle", False):
+            stall["persist_recycled_files"] = store.recycled_files
         stall["persist_tier"] = "off (diagnostic)" if args.stall_no_persist else \
             (f"off ({persist_dropped})" if persist_dropped else
              ("on" if store is not None else "none configured"))
