@@ -235,6 +235,10 @@ SHM_VERSIONS_IN_FLIGHT = 3
 # persist bandwidth): the first ones pay tmpfs page allocation, the last one
 # is the steady-state cost
 PERSIST_PROBE_VERSIONS = 3
+# then versions checkpointed back to back (drain and persist overlapping as in
+# training); their rates, times CADENCE_MARGIN, set the policy's I_ckpt floor
+SUSTAINED_PROBE_VERSIONS = 4
+CADENCE_MARGIN = 1.1
 
 
 def tmpfs_room(root, need_bytes: int, margin: float = 1.05):
@@ -761,7 +765,7 @@ def run_b200(args):
     from paper_2408_04307_b200 import device as D
     from paper_2408_04307_b200.arena import StateArena
     from paper_2408_04307_b200.counting import DeviceTokenCounters
-    from paper_2408_04307_b200.policy import b200_cadence, b200_configure, drain_bandwidth
+    from paper_2408_04307_b200.policy import b200_cadence, b200_configure
     from paper_2408_04307_b200.snapshot import PecCheckpointer
     from paper_2408_04307_b200.store import DiskStore
 
@@ -1022,16 +1026,47 @@ def run_b200(args):
                             "seconds_per_probe_version": [round(x, 3) for x in probe_s],
                             "what": f"{PERSIST_PROBE_VERSIONS} versions, retention between "
                                     "them; seconds/GBps = the last (steady) one"}
+            # sustained: checkpoints issued back to back, so every persist
+            # overlaps the next drain(s) as in the training loop (they share
+            # the host memory); the policy's floors come from these rates
+            ret = Retention(store, ranks=[rank], coordinator=rank == 0)
+            np0, nd0 = len(eng.stats["persist_s"]), len(eng.stats["drain_ms"])
+            barrier(world)
+            ts = time.perf_counter()
+            for j in range(SUSTAINED_PROBE_VERSIONS):
+                ck.checkpoint(base_it + n_e2e + 1 + PERSIST_PROBE_VERSIONS + j)
+                ret.submit()
+            ck.finish()
+            cycle_s = (time.perf_counter() - ts) / SUSTAINED_PROBE_VERSIONS
+            ret.close()
+            barrier(world)
+            prune_store(store, ranks=[rank], coordinator=rank == 0)
+            sus_p = eng.stats["persist_s"][np0:]
+            sus_d = [m / 1e3 for m in eng.stats["drain_ms"][nd0:]]
+            persist_info["sustained"] = {
+                "versions": SUSTAINED_PROBE_VERSIONS,
+                "persist_s": [round(x, 3) for x in sus_p],
+                "drain_s": [round(x, 3) for x in sus_d],
+                "cycle_s": round(cycle_s, 3),
+                "what": "back-to-back checkpoints: persist and drain rates under each other's "
+                        "host-memory contention, and the seconds per checkpoint the pipeline "
+                        "sustains; the cadence floors use these x CADENCE_MARGIN"}
 
         # ---- the cadence the policy derives from this run's measurements ------
         if store is not None and not args.no_stall:
+            sus = persist_info["sustained"]
+            nbytes = eng.stats["snap_bytes"][-1]
+            # slowest rank, under contention, with a margin: a floor computed
+            # with zero slack waits on every variance (simulator.py:413-422)
+            p_eff = CADENCE_MARGIN * max(statistics.mean(sus["persist_s"][1:] or
+                                                         sus["persist_s"]), 1e-9)
+            d_eff = CADENCE_MARGIN * max(statistics.mean(sus["drain_s"][1:] or
+                                                         sus["drain_s"]), 1e-9)
             cl = replace(layout.cluster,
                          snapshot_bandwidth=min_over_ranks(pack_bw, world, dev),
-                         persist_bandwidth=min_over_ranks(
-                             eng.stats["snap_bytes"][-1] / eng.stats["persist_s"][-1],
-                             world, dev),
+                         persist_bandwidth=min_over_ranks(nbytes / p_eff, world, dev),
                          fb_time=args.fb_ms / 1e3, update_time=args.update_ms / 1e3)
-            dbw = min_over_ranks(drain_bandwidth(eng.stats), world, dev)
+            dbw = min_over_ranks(nbytes / d_eff, world, dev)
             cad = b200_cadence(layout, w.strategy, w.pec, cl, dbw)
             cadence = {"i_ckpt_requested": args.i_ckpt, "i_ckpt_min": cad.i_ckpt_min,
                        "feasible": cad.i_ckpt_min <= args.i_ckpt,
@@ -1039,11 +1074,13 @@ def run_b200(args):
                                   "snapshot_overlap": cad.snapshot_floor},
                        "persist_s": round(cad.persist_s, 3), "drain_s": round(cad.drain_s, 3),
                        "pack_ms": round(cad.pack_s * 1e3, 3),
-                       "measured_GBps": {"pack": round(cl.snapshot_bandwidth / 1e9, 1),
+                       "floor_GBps": {"pack": round(cl.snapshot_bandwidth / 1e9, 1),
                                          "drain": round(dbw / 1e9, 2),
                                          "persist": round(cl.persist_bandwidth / 1e9, 2)},
-                       "what": "policy.b200_cadence on this run's slowest-rank pack / drain / "
-                               "persist rates, F&B + update proxy times"}
+                       "margin": CADENCE_MARGIN,
+                       "what": "policy.b200_cadence on this run's slowest-rank pack rate and "
+                               "sustained drain / persist rates (back-to-back checkpoints, "
+                               "x margin), F&B + update proxy times"}
             try:
                 free = b200_configure(layout, w.strategy, cl, dbw)
                 cadence["policy_free_choice"] = {"k_snapshot": free.pec.k_snapshot,
