@@ -31,6 +31,7 @@ from __future__ import annotations
 import argparse
 import importlib
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -239,6 +240,10 @@ PERSIST_PROBE_VERSIONS = 3
 # training); their rates, times CADENCE_MARGIN, set the policy's I_ckpt floor
 SUSTAINED_PROBE_VERSIONS = 4
 CADENCE_MARGIN = 1.1
+# the stall leg's runtime check of that cadence: up to CADENCE_TRIALS short
+# checkpointed runs of TRIAL_CHECKPOINTS checkpoints; any host wait -> I_ckpt x4/3
+CADENCE_TRIALS = 3
+TRIAL_CHECKPOINTS = 4
 
 
 def tmpfs_room(root, need_bytes: int, margin: float = 1.05):
@@ -667,7 +672,8 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
     retention = Retention(store, ranks=[rank], coordinator=rank == 0) \
         if store is not None else None
 
-    def run(with_ckpt: bool, base_it: int):
+    def run(with_ckpt: bool, base_it: int, i_ckpt: int = i_ckpt, n_ckpt: int = n_ckpt):
+        iters = (n_ckpt + 1) * i_ckpt
         barrier(world)
         torch.cuda.synchronize()
         w0 = {k: list(v) for k, v in ck.waits.items()}
@@ -709,10 +715,30 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
     # checkpoint c = iteration // i_ckpt - 1 walks the plan's phases in order
     ck.i_ckpt = i_ckpt
     run(False, 0)  # warm
+    # runtime check of the policy's cadence: a short checkpointed trial; if
+    # any rank waited on a drain or for a persist-freed buffer, I_ckpt grows
+    # by a third and the trial repeats (the policy's rates come from probes
+    # without the training loop, which also contends for the GPU and host)
+    trials = []
+    if store is not None:
+        for t in range(CADENCE_TRIALS):
+            # iterations stay increasing: e2e/probe legs ~1e6, trials here, rounds >= 1e7
+            _, tw, _, _ = run(True, i_ckpt * 10 ** 5 * (t + 2), i_ckpt=i_ckpt,
+                              n_ckpt=TRIAL_CHECKPOINTS)
+            n_wait = int(max_over_ranks(float(tw["snap"][0] + tw["buffer"][0]), world, dev))
+            trials.append({"i_ckpt": i_ckpt, "host_waits": n_wait})
+            if n_wait == 0:
+                break
+            i_ckpt = int(math.ceil(i_ckpt * 4 / 3))
+            ck.i_ckpt = i_ckpt
+            if rank == 0:
+                print(f"bench: {n_wait} host waits in the cadence trial; I_ckpt -> {i_ckpt}",
+                      file=sys.stderr)
+    iters = (n_ckpt + 1) * i_ckpt
     runs_without, runs_with, waits_all, persists, hosts = [], [], [], [], []
     for r in range(rounds):
-        runs_without.append(run(False, 0)[0])
-        ms, waits, pers, host = run(True, i_ckpt * 10 ** 6 * (r + 1))
+        runs_without.append(run(False, 0, i_ckpt=i_ckpt)[0])
+        ms, waits, pers, host = run(True, i_ckpt * 10 ** 6 * (r + 1), i_ckpt=i_ckpt)
         runs_with.append(ms)
         waits_all.append(waits)
         persists += pers
@@ -750,6 +776,7 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
                                   "GBps": round(shard / statistics.mean(persists) / 1e9, 2)
                                   if persists else None},
             "window": "every drain and persist of the arm completes inside the timed window",
+            "cadence_trials": trials,
             "retention_backpressure_s": round(retention_wait_s, 3),
             "diag_with_arms": hosts}
 
