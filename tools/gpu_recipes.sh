@@ -92,6 +92,23 @@ case "$recipe" in
       --master-addr 127.0.0.1 --master-port 29553 bench.py --impl reference --gpus $N \
       --steps 2 --warmup 1 2>/dev/null | tail -1 > $O/bench_n${N}_ref.json
     ;;
+  restore)   # restore throughput (26.1 GB from /dev/shm storage, device / host verify)
+    timeout 900 python tools/restore_bench.py > $O/restore_bench_dev.json
+    timeout 900 python tools/restore_bench.py --verify host > $O/restore_bench_host.json
+    timeout 600 python tools/register_probe.py --gb 8 > $O/register_probe.json
+    ;;
+  host)   # host-memory / tmpfs ceilings of the persist tier (run with gpurun --gpus 4)
+    (lscpu; nvidia-smi topo -m) > $O/host_topo.txt 2>&1
+    timeout 600 python tools/host_probe.py --gb 4 --ranks 4 --threads 8 > $O/host_probe.json
+    ;;
+  recycle_ab)   # N=4 bench with and without persist-file recycling (gpurun --gpus 4)
+    timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 \
+      --master-addr 127.0.0.1 --master-port 29601 bench.py --gpus 4 --steps 20 --warmup 5 \
+      > $O/bench_n4_recycle.json
+    timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 \
+      --master-addr 127.0.0.1 --master-port 29602 bench.py --gpus 4 --steps 5 --warmup 3 \
+      --no-cpu --no-recycle > $O/bench_n4_norecycle.json
+    ;;
   soak)   # the GPU suite N times (flake hunting); prints one summary line per run
     N=${2:-10}
     for i in $(seq 1 $N); do
