@@ -368,3 +368,44 @@ def test_native_writer_crash_budget_matches_the_sequential_writer(tmp_path, dire
     ok = DiskStore(tmp_path / "full", io_threads=4, direct_io=direct)
     ok.write_version(1, 5, 0, ents, injector=TruncatingInjector(total + 1), payloads=pay)
     assert ok.load_checkpoint(1) == pay
+
+
+@pytest.mark.parametrize("payload_kind", ["synthetic", "real"])
+def test_crashtest_newest_complete_survives_random_crashes(tmp_path, payload_kind):
+    """The reference's `mocsim crashtest` loop (cli.py:233-269) on this store
+    and its native writer: version 1 complete, version 2 crashed at a random
+    byte budget; the newest complete version is 1 exactly when the write
+    crashed, and it loads CRC-verified with the bytes that were written."""
+    import random
+    import shutil
+    rng = random.Random(7)
+    prng = np.random.default_rng(7)
+    ents = [StoreEntry(f"ew.L0.E{i}" if i < 4 else f"neo.r{i - 4}", i % 2,
+                       f"ew.L0.E{i}" if i < 4 else f"neo.r{i - 4}", 0, 64 if i % 3 else 70_001)
+            for i in range(6)]
+
+    def pay(v):
+        if payload_kind == "synthetic":
+            return None
+        return {e.store_key: prng.bytes(e.stop - e.start) for e in ents}
+
+    for trial in range(60):
+        root = tmp_path / f"t{trial}"
+        st = DiskStore(root, io_threads=3)
+        p1, p2 = pay(1), pay(2)
+        st.write_version(1, 10, 0, ents, payloads=p1)
+        total = st.serialized_size(2, 20, 1, ents, payloads=p2)
+        budget = rng.randint(0, total + 1)
+        try:
+            st.write_version(2, 20, 1, ents, injector=TruncatingInjector(budget), payloads=p2)
+            crashed = False
+        except CrashPoint:
+            crashed = True
+        newest = st.newest_complete()
+        assert newest == (1 if crashed else 2), (trial, budget)
+        got = st.load_checkpoint(newest)
+        want = (p1 if newest == 1 else p2) or {
+            e.store_key: bytes(entry_payload(e.store_key, newest, 10 if newest == 1 else 20))
+            for e in ents}
+        assert got == {k: bytes(v) for k, v in want.items()}
+        shutil.rmtree(root)
