@@ -736,9 +736,15 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
                       file=sys.stderr)
     iters = (n_ckpt + 1) * i_ckpt
     runs_without, runs_with, waits_all, persists, hosts = [], [], [], [], []
+    gpu = torch.cuda.current_device()
+    clk_arms = {"without": [], "with": []}
     for r in range(rounds):
-        runs_without.append(run(False, 0, i_ckpt=i_ckpt)[0])
-        ms, waits, pers, host = run(True, i_ckpt * 10 ** 6 * (r + 1), i_ckpt=i_ckpt)
+        with ClockSampler(gpu, period_s=0.05) as cw:
+            runs_without.append(run(False, 0, i_ckpt=i_ckpt)[0])
+        with ClockSampler(gpu, period_s=0.05) as cc:
+            ms, waits, pers, host = run(True, i_ckpt * 10 ** 6 * (r + 1), i_ckpt=i_ckpt)
+        clk_arms["without"].append(cw.summary()["sm_mhz"])
+        clk_arms["with"].append(cc.summary()["sm_mhz"])
         runs_with.append(ms)
         waits_all.append(waits)
         persists += pers
@@ -777,6 +783,7 @@ def measure_stall(ck, arena, dev, i_ckpt: int, n_ckpt: int, fb_ms: float, rounds
                                   if persists else None},
             "window": "every drain and persist of the arm completes inside the timed window",
             "cadence_trials": trials,
+            "sm_mhz_median_per_arm": clk_arms,
             "retention_backpressure_s": round(retention_wait_s, 3),
             "diag_with_arms": hosts}
 
