@@ -831,6 +831,8 @@ def run_b200(args):
                           len(os.sched_getaffinity(0)), direct_io=args.direct_io,
                           recycle=persist == "shm" and not args.no_recycle)
     mode = {"vec": D.MODE_VEC, "bulk": D.MODE_BULK, "crc": D.MODE_CRC}[args.engine]
+    if args.pack_mode is not None:          # experiments: a pec_pack engine variant
+        mode = args.pack_mode
     # the persist protocol gets its own gloo group (created collectively inside)
     ck = PecCheckpointer(layout, arena, store, w.pec, w.strategy, i_ckpt=1, ranks=[rank],
                          counters=counters, pack_mode=mode, chunk_log2=args.chunk_log2)
@@ -1174,6 +1176,7 @@ def run_b200(args):
                        "bytes_per_step_rank0": moved // args.steps,
                        "state_resident_gb": round(arena.resident_bytes() / 1e9, 2),
                        "engine": args.engine, "chunk_log2": args.chunk_log2,
+                       **({"pack_mode": args.pack_mode} if args.pack_mode is not None else {}),
                        "value_is": "HBM-staged snapshot: selection + pack (+ per-entry CRC-32C) "
                                    "into HBM staging, the training-blocking step; e2e = bytes "
                                    "in pinned host memory (the reference's SNAPSHOTTED)",
@@ -1247,6 +1250,9 @@ def main():
                          "the persist tier then never reads payloads for checksums), plain "
                          "TMA bulk, or LDG/STG vector")
     ap.add_argument("--chunk-log2", type=int, default=15)
+    ap.add_argument("--pack-mode", type=int, default=None,
+                    help="experiments only: a pec_pack mode (engine variant, csrc/pec_kernels.cu "
+                         "launch_copy); CRCs then come from the host writer")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--persist", default="auto", choices=["auto", "none", "shm", "disk"])
     ap.add_argument("--direct-io", action="store_true",
