@@ -224,32 +224,45 @@ __device__ __forceinline__ void bulk_wait_all() {
 }
 
 // ---- shared-memory layout of pack_crc_kernel (dynamic, bytes) --------------
-// ytab     256 entries x 64 words: entry e, table k, lane group g at word
-//          64 e + 32 (k & 1) + 16 (k >> 1) + g   (64 KiB)
-// lanetab  8 x 16 windows x 32 lanes of x^(128 (31 - l))  (16 KiB)
-// nib      4 x 128 windows of x^(32 (4 - t)), t = 0..3   (2 KiB)
-// t8       standard byte table (slow path)                 (1 KiB)
-// x2k      64 words
-// ring     kWarps x kRing x 4 KiB
-// bars     kWarps x kRing mbarriers
+// The Y tables sit at shared-window address kYtabAddr (64 KiB-aligned), so a
+// lookup address is ONE PRMT of (S, slot): byte 0 the lane's bank slot,
+// byte 1 byte k of S, bytes 2-3 the table base carried in the slot register,
+// and the LDS needs no add (PRMT + LDS per lookup instead of PRMT + IADD + LDS).
+//   smem + 0      misc: lanetab 8 x 16 windows x 32 lanes of x^(128 (31 - l))
+//                 (16 KiB), nib 4 x 128 windows of x^(32 (4 - t)) (2 KiB), t8 the
+//                 standard byte table (1 KiB), x2k (256 B)
+//   + kMiscBytes  bars: kWarps x kRing mbarriers
+//   + kPreOff     rings of warps 0 .. kPreRings-1 (kRing x 4 KiB each)
+//   kYtabAddr     ytab 256 entries x 64 words: entry e, table k, lane group g
+//                 at word 64 e + 32 (k & 1) + 16 (k >> 1) + g   (64 KiB)
+//   + 64 KiB      rings of the other warps
 constexpr int kYtabWords = 256 * 64;
 constexpr int kLaneTabWords = 8 * 16 * 32;
 constexpr int kNibWords = 4 * 128;
 static_assert(sizeof(SmemImage) == (size_t)(kYtabWords + kLaneTabWords + kNibWords + 256 + 64) * 4,
               "shared-memory table image layout");
 static_assert(sizeof(SmemImage) % 16 == 0, "TMA bulk copies move multiples of 16 bytes");
-constexpr size_t kSmemBytes = sizeof(SmemImage) +
-                              (size_t)kWarps * kRing * kStage + (size_t)kWarps * kRing * 8;
+constexpr uint32_t kYtabBytes = (uint32_t)kYtabWords * 4;
+constexpr uint32_t kMiscBytes = (uint32_t)sizeof(SmemImage) - kYtabBytes;
+constexpr uint32_t kRingBytes = (uint32_t)kRing * kStage;
+constexpr int kPreRings = 2;
+constexpr uint32_t kPreOff = (kMiscBytes + (uint32_t)kWarps * kRing * 8 + 127) / 128 * 128;
+constexpr uint32_t kYtabAddr = 0x10000;
+static_assert(kPreOff + kPreRings * kRingBytes < kYtabAddr, "ytab placement");
+// worst case (dynamic window starting at shared address 0): up to the end of the last ring
+constexpr size_t kSmemBytes = (size_t)kYtabAddr + kYtabBytes + (size_t)(kWarps - kPreRings) * kRingBytes;
+static_assert(kSmemBytes <= 227 * 1024 - 1024, "dynamic shared memory budget");
+static_assert(kMiscBytes % 16 == 0 && kYtabBytes % 16 == 0, "bulk-copy sizes");
 
-// One chain step S * Y ^ w: four table lookups at PRMT-formed byte offsets
-// (byte k of S into bits 8-15, the lane's slot for step s in bits 0-7).
-__device__ __forceinline__ uint32_t ystep(const uint8_t* ytab, uint32_t S, uint32_t w,
-                                          const uint32_t (&slot)[4], const uint32_t (&sel)[4]) {
+// One chain step S * Y ^ w: four table lookups whose shared addresses are
+// formed by one PRMT each (see the layout above).
+__device__ __forceinline__ uint32_t ystep(uint32_t S, uint32_t w, const uint32_t (&slot)[4],
+                                          const uint32_t (&sel)[4]) {
   uint32_t a[4];
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
-    const uint32_t off = __byte_perm(S, slot[s], sel[s]);
-    a[s] = *reinterpret_cast<const uint32_t*>(ytab + off);
+    const uint32_t addr = __byte_perm(S, slot[s], sel[s]);
+    asm("ld.shared.u32 %0, [%1];" : "=r"(a[s]) : "r"(addr));
   }
   return a[0] ^ a[1] ^ a[2] ^ a[3] ^ w;
 }
@@ -293,13 +306,15 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
                 const uint64_t* __restrict__ total_dev, uint32_t* __restrict__ chunk_raw) {
   const uint64_t total_cap = total;       // scratch is sized for the launch bound
   extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* ytab = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* lanetab = ytab + kYtabWords;
+  const uint32_t sbase = smem_u32(smem);
+  // the layout needs the dynamic window to start below kYtabAddr - kPreOff -
+  // kPreRings rings (it starts after ~2 KiB of static + reserved shared memory)
+  if (sbase + kPreOff + kPreRings * kRingBytes > kYtabAddr) __trap();
+  uint32_t* lanetab = reinterpret_cast<uint32_t*>(smem);
   uint32_t* nib = lanetab + kLaneTabWords;
   uint32_t* t8 = nib + kNibWords;
-  uint32_t* x2k = t8 + 256;
-  uint8_t* ring = reinterpret_cast<uint8_t*>(x2k + 64);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)kWarps * kRing * kStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kMiscBytes);
+  uint8_t* ytab = smem + (kYtabAddr - sbase);
   __shared__ QueueEntry queue[kWarps * kQueue];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -317,7 +332,8 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
   __syncthreads();
   if (tid == 0) {
     mbar_expect_tx(&table_bar, (uint32_t)sizeof(SmemImage));
-    bulk_g2s_plain(smem, &kTab.img, (uint32_t)sizeof(SmemImage), &table_bar);
+    bulk_g2s_plain(ytab, kTab.img.ytab, kYtabBytes, &table_bar);
+    bulk_g2s_plain(smem, kTab.img.lanetab, kMiscBytes, &table_bar);
   }
   mbar_wait(&table_bar, 0);
 
@@ -331,14 +347,15 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
   for (int s = 0; s < 4; ++s) {
     const uint32_t tk = (uint32_t)s ^ (h << 1);
     slot[s] = ((tk & 1u) << 7) | ((tk >> 1) << 6) | (g << 2);
-    sel[s] = 0x6604u | (tk << 4);  // byte0 <- slot, byte1 <- S.byte[tk], bytes 2-3 <- 0
+    slot[s] |= kYtabAddr;          // the table base rides in bytes 2-3
+    sel[s] = 0x7604u | (tk << 4);  // byte0 <- slot, byte1 <- S.byte[tk], bytes 2-3 <- slot
   }
-  const uint8_t* yb = reinterpret_cast<const uint8_t*>(ytab);
   const uint32_t* ltab = lanetab + lane;
 
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-  uint8_t* my_ring = ring + (size_t)warp * kRing * kStage;
+  uint8_t* my_ring = warp < kPreRings ? smem + kPreOff + (size_t)warp * kRingBytes
+                                       : ytab + kYtabBytes + (size_t)(warp - kPreRings) * kRingBytes;
   uint64_t* my_bars = bars + warp * kRing;
   QueueEntry* q = queue + warp * kQueue;
   // chunks are claimed dynamically from a counter (slot `total` of the
@@ -425,10 +442,10 @@ pack_crc_kernel(const pec_copy_desc* __restrict__ d, int n, uint64_t total,
 #pragma unroll
         for (int j = 0; j < kRowsPerStage; ++j) {
           const int4 v = rows[32 * j];
-          S0 = ystep(yb, S0, (uint32_t)v.x, slot, sel);
-          S1 = ystep(yb, S1, (uint32_t)v.y, slot, sel);
-          S2 = ystep(yb, S2, (uint32_t)v.z, slot, sel);
-          S3 = ystep(yb, S3, (uint32_t)v.w, slot, sel);
+          S0 = ystep(S0, (uint32_t)v.x, slot, sel);
+          S1 = ystep(S1, (uint32_t)v.y, slot, sel);
+          S2 = ystep(S2, (uint32_t)v.z, slot, sel);
+          S3 = ystep(S3, (uint32_t)v.w, slot, sel);
         }
         __syncwarp();            // every lane has read the stage
         ++consumed;
