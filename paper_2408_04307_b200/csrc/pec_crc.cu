@@ -13,7 +13,7 @@
 // crc(M) = ~(R(M) ^ ~0 * x^(8|M|) mod P).
 //
 // pack_crc_kernel (one persistent CTA per SM, 8 warps, each warp owns whole
-// 32 KiB chunks, chunk c -> warp c mod #warps):
+// 32 KiB chunks, claimed one at a time from a counter so faster SMs take more):
 //   * each warp streams its chunks as 4 KiB stages through its own ring in
 //     shared memory: lane 0 issues cp.async.bulk global->smem (mbarrier
 //     complete_tx), then cp.async.bulk smem->global into staging — the bytes
@@ -27,8 +27,9 @@
 //     live in shared memory replicated 16x, tables 0/1 in banks 0-15 and
 //     2/3 in banks 16-31, and the upper half-warp visits the byte positions
 //     in the order 2,3,0,1 — so every lookup of a warp hits 32 distinct
-//     banks.  A PRMT forms each lookup address (byte of S in bits 8-15, the
-//     lane's bank slot in bits 0-7): 2 instructions per lookup;
+//     banks.  A PRMT forms each whole lookup address (byte of S in bits 8-15,
+//     the lane's bank slot in bits 0-7, the tables' 64 KiB-aligned shared
+//     base in bits 16-31): 2 instructions per lookup (PRMT + LDS);
 //   * per chunk, lane l joins its chains (x^(32 (4 - t))) and shifts by its
 //     lane constant x^(128 (31 - l)); a XOR butterfly gives R(chunk).
 //   Chunks that are partial (an entry's last) or not 16-byte aligned take a
@@ -39,7 +40,8 @@
 //   the final inversion per entry.
 // Multiplication mod P (reflected, bit 31 = x^0) is the shift-and-add
 // schoolbook product or, for constants, 8 lookups of 4-bit-window tables;
-// x^(2^k) are precomputed on the host.
+// every table and power (x^(2^k), chunk and byte powers) is computed by the
+// compiler (constexpr make_tables) into the device image.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
